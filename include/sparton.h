@@ -1,0 +1,107 @@
+/*
+ * sparton.h — C ABI of the B200-native fused SPLADE LM head ("Sparton").
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/fusedhead/fused.py).  Every entry point takes plain
+ * device pointers, explicit sizes / leading dimensions and a cudaStream_t
+ * (passed as void*), so any host language can bind it (ctypes, cgo, JNI, ...).
+ * No torch types cross this boundary.
+ *
+ * Semantics (identical to the reference):
+ *   L[b,s,v] = (sum_k H[b,s,k] * E[v,k] + bias[v]) * mask[b,s]     (masked -> exactly 0)
+ *   I[b,v]   = smallest s attaining max_s L[b,s,v]                  (int32)
+ *   Y[b,v]   = log1p(max(L[b,I[b,v],v], 0))                         (float32)
+ *   g[b,v]   = dY[b,v] * exp(-Y[b,v])  if Y[b,v] > 0 else 0
+ *   dE[v,:]  = sum_b g[b,v] * H[b, I[b,v], :]     (b ascending, single owner)
+ *   db[v]    = sum_b g[b,v]                       (b ascending, single owner)
+ *   dH[b,s,:]= sum_{v : I[b,v]=s} g[b,v] * E[v,:] (v ascending, single owner)
+ *
+ * Layout: H is (B*S) x D row-major bf16 (ld = D), E is V x D row-major bf16,
+ * bias f32[V], mask u8[B*S] in {0,1}, Y f32 / I i32 are B x ldY (ldY >= V).
+ * H and E must be 16-byte aligned and D a multiple of 8 (TMA stride rule);
+ * callers with other D zero-pad the K axis (zero columns add exactly 0).
+ *
+ * All calls are stream-ordered and asynchronous; outputs and workspace are
+ * caller-owned (kernels never allocate).  Only shapes, dtypes and alignment
+ * are validated — no device-side value scans — mirroring backward_fused's
+ * deliberate "validate shapes only" contract (fused.py:232-245).
+ */
+#ifndef SPARTON_H_
+#define SPARTON_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define SPARTON_API __attribute__((visibility("default")))
+#else
+#define SPARTON_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The Python layer maps EINVAL -> ValueError (the reference's
+ * shape/dtype errors, reference.py:32-46, fused.py:240-245) and ECUDA /
+ * ENOTSUP -> RuntimeError. */
+enum {
+  SPARTON_OK = 0,
+  SPARTON_EINVAL = 1,   /* bad shape / leading dim / alignment / null pointer */
+  SPARTON_ECUDA = 2,    /* a CUDA runtime / driver call failed               */
+  SPARTON_ENOTSUP = 3   /* device is not sm_100 (B200)                      */
+};
+
+/* Gradient output element types for sparton_bwd. */
+enum { SPARTON_F32 = 0, SPARTON_BF16 = 1 };
+
+/* ABI version (major*100 + minor). */
+SPARTON_API int sparton_abi_version(void);
+
+/* Thread-local description of the last non-OK status on this thread. */
+SPARTON_API const char* sparton_last_error(void);
+
+/* Number of SMs of the current device (0 when no device) — lets hosts size
+ * shards; pure query, no kernel launch. */
+SPARTON_API int sparton_device_sm_count(void);
+
+/*
+ * Forward.  Replaces forward_fully_fused / forward_hybrid
+ * (fused.py:160-212 / fused.py:115-157): one persistent sm_100a kernel
+ * (TMA -> tcgen05.mma bf16 -> TMEM fp32 -> fused bias/mask/max/argmax/log1p
+ * epilogue).  Writes only Y and I; the B*S*V logits are never materialised.
+ *   H     : bf16 [B*S, D]       E    : bf16 [V, D]
+ *   bias  : f32 [V]             mask : u8 [B*S] (row-major B x S)
+ *   Y     : f32 [B, ldY]        I    : i32 [B, ldY]
+ *   cta_group : 0 = auto, 1 = single-CTA UMMA (M=128), 2 = CTA pair (M=256)
+ */
+SPARTON_API int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* mask,
+                float* Y, int32_t* I,
+                int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY,
+                int cta_group, void* stream);
+
+/* Workspace bytes sparton_bwd needs for these sizes (argmax-routed pair lists
+ * for dH: B*V*8 bytes + offsets).  Pure host arithmetic. */
+SPARTON_API size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t V);
+
+/*
+ * Backward.  Replaces backward_fused (fused.py:215-278) from the saved
+ * (Y, I) only.  dH/dE/db are fully overwritten (no accumulation into caller
+ * buffers).  db may be NULL or include_bias_grad = 0 (fused.py:221,264) in
+ * which case it is written as zeros if non-NULL.  Deterministic: every output
+ * element has a single owner that accumulates in the reference's order.
+ *   dY : f32 [B, ldDY]    dH : [B*S, D]   dE : [V, D]   db : f32 [V]
+ *   grad_dtype : SPARTON_F32 or SPARTON_BF16 for dH and dE.
+ *   workspace  : >= sparton_bwd_workspace_bytes(B, S, V) bytes, 16-B aligned.
+ */
+SPARTON_API int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I,
+                const float* dY, void* dH, void* dE, float* db,
+                int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int64_t ldDY,
+                int include_bias_grad, int grad_dtype,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif  /* SPARTON_H_ */

@@ -1,0 +1,24 @@
+"""paper_2603_25011_b200 — B200-native fused SPLADE LM head (Sparton).
+
+The hot path of arXiv 2603.25011 built from scratch for sm_100a:
+``Y = log1p(relu(max_s((H·Eᵀ + b) ⊙ M)))`` plus int32 argmax, forward in one
+tcgen05/TMEM/TMA kernel, backward in deterministic argmax-routed gather
+kernels, behind the C ABI of ``include/sparton.h``.
+
+Public surface:
+  * torch:  ``sparton_forward``, ``sparton_backward``, ``SpartonHeadFn``, ``sparton_head``
+  * reference-API mirror (numpy in/out): ``paper_2603_25011_b200.fusedhead``
+  * vocab-sharded multi-GPU head: ``paper_2603_25011_b200.sharded``
+"""
+
+from .head import SpartonHeadFn, bwd_workspace_bytes, sparton_backward, sparton_forward, sparton_head
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "SpartonHeadFn",
+    "bwd_workspace_bytes",
+    "sparton_backward",
+    "sparton_forward",
+    "sparton_head",
+]

@@ -1,0 +1,229 @@
+// sparton_abi.cu — the C-ABI entry points declared in include/sparton.h.
+//
+// Host-side validation mirrors the reference's error contract
+// (reference.py:32-46 shape/dtype checks; fused.py:240-245 backward shape
+// checks) but, like backward_fused (fused.py:232-235), never scans values.
+// TMA tensor maps are encoded per call through the driver entry point
+// obtained from the runtime (no link-time dependency on libcuda, so the
+// library loads on GPU-less hosts for symbol checks).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "sparton_internal.h"
+
+namespace sparton {
+
+namespace {
+thread_local char g_err[512] = "";
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int major = 0;
+  int minor = 0;
+};
+
+int device_info(DevInfo& out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error("cudaGetDevice", e);
+  static DevInfo cache[64];
+  static bool have[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && have[dev]) { out = cache[dev]; return SPARTON_OK; }
+  DevInfo d;
+  if ((e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess ||
+      (e = cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess ||
+      (e = cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev)) != cudaSuccess)
+    return set_cuda_error("cudaDeviceGetAttribute", e);
+  if (dev < 64) { cache[dev] = d; have[dev] = true; }
+  out = d;
+  return SPARTON_OK;
+}
+
+int encode_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols,
+                   int box_rows, int box_cols) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return set_error(SPARTON_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (CUresult %d) rows=%lld cols=%lld",
+             (int)r, rows, cols);
+    return set_error(SPARTON_ECUDA, buf);
+  }
+  return SPARTON_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+int set_error(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+
+int set_cuda_error(const char* what, cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  return SPARTON_ECUDA;
+}
+
+}  // namespace sparton
+
+using namespace sparton;
+
+extern "C" {
+
+int sparton_abi_version(void) { return 100; }
+
+const char* sparton_last_error(void) { return g_err; }
+
+int sparton_device_sm_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  DevInfo d;
+  if (device_info(d) != SPARTON_OK) return 0;
+  return d.sms;
+}
+
+static int check_dims(int64_t B, int64_t S, int64_t D, int64_t V) {
+  char buf[200];
+  if (B < 1 || S < 1 || D < 1 || V < 1) {
+    snprintf(buf, sizeof(buf), "dims must be positive, got B=%lld S=%lld D=%lld V=%lld",
+             (long long)B, (long long)S, (long long)D, (long long)V);
+    return set_error(SPARTON_EINVAL, buf);
+  }
+  if (D % 8 != 0) {
+    snprintf(buf, sizeof(buf), "D=%lld must be a multiple of 8 (zero-pad the hidden axis)", (long long)D);
+    return set_error(SPARTON_EINVAL, buf);
+  }
+  if (B * S >= (1ll << 31) || V >= (1ll << 31) || B * V >= (1ll << 40) || D > (1 << 20)) {
+    snprintf(buf, sizeof(buf), "dims exceed the kernel's index range: B=%lld S=%lld D=%lld V=%lld",
+             (long long)B, (long long)S, (long long)D, (long long)V);
+    return set_error(SPARTON_EINVAL, buf);
+  }
+  return SPARTON_OK;
+}
+
+static int check_device() {
+  DevInfo d;
+  int rc = device_info(d);
+  if (rc != SPARTON_OK) return rc;
+  if (d.major != 10 || d.minor != 0) {
+    char buf[128];
+    snprintf(buf, sizeof(buf), "sparton kernels are built for sm_100a (B200); device is sm_%d%d",
+             d.major, d.minor);
+    return set_error(SPARTON_ENOTSUP, buf);
+  }
+  return SPARTON_OK;
+}
+
+int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* mask, float* Y,
+                int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int cta_group,
+                void* stream) {
+  int rc = check_dims(B, S, D, V);
+  if (rc) return rc;
+  if (!H || !E || !bias || !mask || !Y || !I) return set_error(SPARTON_EINVAL, "null pointer argument");
+  if (!aligned16(H) || !aligned16(E)) return set_error(SPARTON_EINVAL, "H and E must be 16-byte aligned");
+  if (ldY < V) return set_error(SPARTON_EINVAL, "ldY must be >= V");
+  if (cta_group < 0 || cta_group > 2) return set_error(SPARTON_EINVAL, "cta_group must be 0, 1 or 2");
+  if ((rc = check_device())) return rc;
+  DevInfo d;
+  device_info(d);
+  const int cg = cta_group == 0 ? 2 : cta_group;
+  CUtensorMap tmE, tmH;
+  if ((rc = encode_bf16_2d(&tmE, E, V, D, 128, 64))) return rc;
+  if ((rc = encode_bf16_2d(&tmH, H, B * S, D, 256 / cg, 64))) return rc;
+  FwdParams prm = {};
+  prm.bias = bias;
+  prm.mask = mask;
+  prm.Y = Y;
+  prm.I = I;
+  prm.B = (int)B;
+  prm.S = (int)S;
+  prm.D = (int)D;
+  prm.V = (int)V;
+  prm.ldY = ldY;
+  return launch_fwd(tmE, tmH, prm, cg, d.sms, static_cast<cudaStream_t>(stream));
+}
+
+size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t V) {
+  if (B < 1 || S < 1 || V < 1) return 0;
+  return bwd_workspace_bytes(B, S, V);
+}
+
+int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, const float* dY,
+                void* dH, void* dE, float* db, int64_t B, int64_t S, int64_t D, int64_t V,
+                int64_t ldY, int64_t ldDY, int include_bias_grad, int grad_dtype, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  int rc = check_dims(B, S, D, V);
+  if (rc) return rc;
+  if (!H || !E || !Y || !I || !dY || !dH || !dE || !workspace)
+    return set_error(SPARTON_EINVAL, "null pointer argument");
+  if (!aligned16(H) || !aligned16(E) || !aligned16(dH) || !aligned16(dE) || !aligned16(workspace))
+    return set_error(SPARTON_EINVAL, "H, E, dH, dE and workspace must be 16-byte aligned");
+  if (ldY < V || ldDY < V) return set_error(SPARTON_EINVAL, "ldY and ldDY must be >= V");
+  if (grad_dtype != SPARTON_F32 && grad_dtype != SPARTON_BF16)
+    return set_error(SPARTON_EINVAL, "grad_dtype must be SPARTON_F32 or SPARTON_BF16");
+  if (S > bwd_max_seq()) return set_error(SPARTON_EINVAL, "S exceeds the backward's routing limit");
+  const size_t need = bwd_workspace_bytes(B, S, V);
+  if (workspace_bytes < need) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+    return set_error(SPARTON_EINVAL, buf);
+  }
+  if ((rc = check_device())) return rc;
+  BwdParams p = {};
+  p.H = static_cast<const __nv_bfloat16*>(H);
+  p.E = static_cast<const __nv_bfloat16*>(E);
+  p.Y = Y;
+  p.I = I;
+  p.dY = dY;
+  p.dH = dH;
+  p.dE = dE;
+  p.db = db;
+  p.B = (int)B;
+  p.S = (int)S;
+  p.D = (int)D;
+  p.V = (int)V;
+  p.ldY = ldY;
+  p.ldDY = ldDY;
+  p.include_bias_grad = include_bias_grad;
+  const size_t pairs_bytes = ((size_t)B * (size_t)V * sizeof(int2) + 255) & ~size_t(255);
+  p.pairs = static_cast<int2*>(workspace);
+  p.offsets = reinterpret_cast<int*>(static_cast<char*>(workspace) + pairs_bytes);
+  return launch_bwd(p, grad_dtype, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

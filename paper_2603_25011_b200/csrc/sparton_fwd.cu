@@ -1,0 +1,335 @@
+// sparton_fwd.cu — K1: the fused Sparton LM-head forward on sm_100a.
+//
+// Replaces the reference's forward_fully_fused / forward_hybrid
+// (/root/reference/pkg/src/fusedhead/fused.py:160-212 and :115-157) and the
+// GEMM stage matmul_bt (tensor.py:130-188).  One persistent, warp-specialised
+// kernel per call:
+//
+//   warp 0        TMA producer: E tile (vocab rows, K-major) and H tile
+//                 (sequence rows of one batch row, K-major) -> smem ring.
+//   warp 1        TMEM allocator; on the leader CTA, the single-thread
+//                 tcgen05.mma issuer (bf16 x bf16 -> f32 in TMEM).
+//   warps 2..5    epilogue: tcgen05.ld the accumulator, add bias, apply the
+//                 mask (masked -> exactly 0, out-of-range s -> skipped), and
+//                 keep a running (max, first argmax) per vocab row in
+//                 registers across sequence chunks; log1p(relu(.)) is applied
+//                 once per (b, v) after the reduction (fused.py:203).
+//
+// Work unit = (batch row b, vocab tile of 128*CG rows); the unit loops over
+// sequence chunks of 256 positions.  UMMA shape M = 128*CG (vocab on TMEM
+// lanes, one lane per vocab row), N = 256 (sequence positions), K = 16.
+// Each epilogue thread owns one vocab row and scans its columns in s order,
+// so the strict '>' update reproduces the reference's smallest-index tie
+// rule (fused.py:200) without cross-lane reductions.
+// TMEM holds two 256-column accumulators so the epilogue of chunk i overlaps
+// the MMAs of chunk i+1.  CG=2 runs a CTA pair (cta_group::2): each CTA loads
+// half of the E tile and half of the H tile, the leader issues M=256 MMAs.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cmath>
+
+#include "ptx.cuh"
+#include "sparton_internal.h"
+
+namespace sparton {
+
+template <int CG>
+struct FwdCfg {
+  static constexpr int BM = 128;                 // vocab rows per CTA (TMEM lanes)
+  static constexpr int TILE_V = BM * CG;         // vocab rows per unit
+  static constexpr int SN = 256;                 // sequence positions per chunk (UMMA N)
+  static constexpr int BN_CTA = SN / CG;         // H rows each CTA loads per chunk
+  static constexpr int BK = 64;                  // K per stage = one 128-B swizzle row
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN_CTA * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int NST = CG == 1 ? 4 : 6;
+  static constexpr int UMMA_M = BM * CG;
+  static constexpr int NUM_THREADS = 192;
+  static constexpr int TMEM_COLS = 512;          // 2 accumulators x 256 columns
+  static constexpr int SMEM_BYTES = NST * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void unit_coords(long long u, const FwdParams& p, int& b, int& vt) {
+  const long long per_group = (long long)p.group_vt * p.B;
+  const long long g = u / per_group;
+  const long long r = u - g * per_group;
+  const int gv0 = (int)g * p.group_vt;
+  const int gsz = min(p.group_vt, p.num_vt - gv0);
+  b = (int)(r / gsz);
+  vt = gv0 + (int)(r % gsz);
+}
+
+// Reduce 32 accumulator columns (tile columns c0..c0+31 of the current chunk)
+// into four interleaved running (max, argmax) pairs; column c goes to slot c&3.
+// `keep` bit l: position valid and unmasked (value = acc + bias);
+// `zero` bit l: position valid but masked (value = 0, still competes);
+// neither: position beyond S (skipped).
+__device__ __forceinline__ void reduce_group(const float (&r)[32], float bias, uint32_t keep,
+                                             uint32_t zero, int c0, float (&best)[4],
+                                             int (&bidx)[4]) {
+  if (keep == 0xffffffffu) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const float x = r[c] + bias;
+      if (x > best[c & 3]) { best[c & 3] = x; bidx[c & 3] = c0 + c; }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      float x = r[c] + bias;
+      x = ((keep >> c) & 1u) ? x : (((zero >> c) & 1u) ? 0.0f : -INFINITY);
+      if (x > best[c & 3]) { best[c & 3] = x; bidx[c & 3] = c0 + c; }
+    }
+  }
+}
+
+template <int CG>
+__global__ void __launch_bounds__(FwdCfg<CG>::NUM_THREADS, 1)
+sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmH,
+                   const FwdParams p) {
+  using C = FwdCfg<CG>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment for the 128-B swizzle atoms.
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::NST * C::STAGE_BYTES);
+  uint64_t* full = bars;                   // [NST]
+  uint64_t* empty = bars + C::NST;         // [NST]
+  uint64_t* tfull = bars + 2 * C::NST;     // [2]
+  uint64_t* tempty = bars + 2 * C::NST + 2;// [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::NST + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
+  const long long cluster = (CG == 2) ? (long long)ptx::cluster_id_x() : (long long)blockIdx.x;
+  const long long nclusters = (CG == 2) ? (long long)ptx::nclusters_x() : (long long)gridDim.x;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmE);
+    ptx::prefetch_tmap(&tmH);
+    for (int i = 0; i < C::NST; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&tfull[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&tempty[i]), 4 * CG);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<CG>(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nsc = (p.S + C::SN - 1) / C::SN;
+  const int nkb = (p.D + C::BK - 1) / C::BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      const uint64_t pol_e = ptx::policy_evict_last();
+      const uint64_t pol_h = ptx::policy_evict_normal();
+      int st = 0;
+      uint32_t ph = 0;
+      for (long long u = cluster; u < p.num_units; u += nclusters) {
+        int b, vt;
+        unit_coords(u, p, b, vt);
+        const int vrow = vt * C::TILE_V + (int)rank * C::BM;
+        for (int sc = 0; sc < nsc; ++sc) {
+          const int hrow = b * p.S + sc * C::SN + (int)rank * C::BN_CTA;
+          for (int kb = 0; kb < nkb; ++kb) {
+            ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
+            const uint32_t sa = ptx::smem_u32(stage_base + st * C::STAGE_BYTES);
+            const uint32_t sb = sa + C::A_BYTES;
+            const uint32_t fb = ptx::smem_u32(&full[st]);
+            if constexpr (CG == 1) {
+              ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+              ptx::tma_load_2d(&tmE, sa, fb, kb * C::BK, vrow, pol_e);
+              ptx::tma_load_2d(&tmH, sb, fb, kb * C::BK, hrow, pol_h);
+            } else {
+              if (rank == 0) ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES * 2);
+              ptx::tma_load_2d_cg2(&tmE, sa, fb, kb * C::BK, vrow, pol_e);
+              ptx::tma_load_2d_cg2(&tmH, sb, fb, kb * C::BK, hrow, pol_h);
+            }
+            if (++st == C::NST) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
+      int st = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (long long u = cluster; u < p.num_units; u += nclusters) {
+        for (int sc = 0; sc < nsc; ++sc) {
+          ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), aph ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t dt = tmem_base + (uint32_t)(acc * C::SN);
+          for (int kb = 0; kb < nkb; ++kb) {
+            ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
+            ptx::tc_fence_after();
+            const uint32_t sa = ptx::smem_u32(stage_base + st * C::STAGE_BYTES);
+            const uint64_t da = ptx::umma_desc_sw128(sa);
+            const uint64_t db = ptx::umma_desc_sw128(sa + C::A_BYTES);
+#pragma unroll
+            for (int k = 0; k < C::BK / 16; ++k) {
+              // +32 bytes along K inside the 128-B swizzle row = +2 in the >>4 address field.
+              ptx::umma_bf16<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            }
+            ptx::umma_commit<CG>(ptx::smem_u32(&empty[st]));
+            if (++st == C::NST) { st = 0; ph ^= 1; }
+          }
+          ptx::umma_commit<CG>(ptx::smem_u32(&tfull[acc]));
+          acc ^= 1;
+          if (acc == 0) aph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;                       // TMEM lane quarter this warp may access
+    const int row = q * 32 + (int)lane;           // vocab row within this CTA's tile
+    const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
+    uint32_t tempty_addr[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t a = ptx::smem_u32(&tempty[i]);
+      tempty_addr[i] = (CG == 2) ? ptx::mapa(a, 0) : a;
+    }
+    int acc = 0;
+    uint32_t aph = 0;
+    for (long long u = cluster; u < p.num_units; u += nclusters) {
+      int b, vt;
+      unit_coords(u, p, b, vt);
+      const int v = vt * C::TILE_V + (int)rank * C::BM + row;
+      const float bv = (v < p.V) ? __ldg(p.bias + v) : 0.0f;
+      const uint8_t* mrow = p.mask + (size_t)b * p.S;
+      float best = -INFINITY;
+      int bidx = 0;
+      for (int sc = 0; sc < nsc; ++sc) {
+        const int s0 = sc * C::SN;
+        // Mask words for the 8 column groups of this chunk (warp-uniform).
+        uint32_t keep[8], zero[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int s = s0 + j * 32 + (int)lane;
+          const bool valid = s < p.S;
+          const bool m = valid && (__ldg(mrow + (valid ? s : 0)) != 0);
+          keep[j] = __ballot_sync(0xffffffffu, m);
+          zero[j] = __ballot_sync(0xffffffffu, valid && !m);
+        }
+        ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), aph);
+        ptx::tc_fence_after();
+        float cb[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int ci[4] = {0, 0, 0, 0};
+        const uint32_t tacc = tq + (uint32_t)(acc * C::SN);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float r[32];
+          ptx::tmem_ld32(tacc + (uint32_t)(j * 32), r);
+          ptx::tmem_ld_wait();
+          ptx::reg_fence32(r);
+          if ((keep[j] | zero[j]) != 0u) reduce_group(r, bv, keep[j], zero[j], j * 32, cb, ci);
+        }
+        // Accumulator fully read: hand it back to the MMA warp.
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster(tempty_addr[acc]);
+          else ptx::mbar_arrive(tempty_addr[acc]);
+        }
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+        // Merge the four interleaved slots: larger value wins, equal values keep the
+        // smaller column (first occurrence), then fold into the running pair with a
+        // strict '>' (earlier chunks hold smaller s).
+        float m = cb[0];
+        int mi = ci[0];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) {
+          if (cb[k] > m || (cb[k] == m && ci[k] < mi)) { m = cb[k]; mi = ci[k]; }
+        }
+        if (m > best) { best = m; bidx = s0 + mi; }
+      }
+      if (v < p.V) {
+        const size_t o = (size_t)b * (size_t)p.ldY + (size_t)v;
+        p.Y[o] = log1pf(fmaxf(best, 0.0f));
+        p.I[o] = bidx;
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+template <int CG>
+int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdParams& prm,
+                    int num_sms, cudaStream_t stream) {
+  using C = FwdCfg<CG>;
+  auto kern = sparton_fwd_kernel<CG>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(fwd)", e);
+  long long want = prm.num_units;
+  int grid = num_sms;                    // persistent: one CTA per SM
+  if (CG == 2) grid = (num_sms / 2) * 2;
+  if (want < grid / CG) grid = (int)want * CG;
+  if (grid < CG) grid = CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (CG == 2) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    na = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  e = cudaLaunchKernelEx(&cfg, kern, tmE, tmH, prm);
+  if (e != cudaSuccess) return set_cuda_error("launch sparton_fwd_kernel", e);
+  return SPARTON_OK;
+}
+
+int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cta_group,
+               int num_sms, cudaStream_t stream) {
+  const int tile_v = 128 * cta_group;
+  prm.num_vt = (prm.V + tile_v - 1) / tile_v;
+  // L2 rasterisation: walk a group of vocab tiles (~24 MB of E) for every batch
+  // row before moving on, so the group of E stays L2-resident while H[b] is
+  // shared by all CTAs working on the same b.
+  long long tile_bytes = (long long)tile_v * prm.D * 2;
+  int gv = (int)((24ll << 20) / (tile_bytes > 0 ? tile_bytes : 1));
+  if (gv < 1) gv = 1;
+  if (gv > prm.num_vt) gv = prm.num_vt;
+  prm.group_vt = gv;
+  prm.num_units = (long long)prm.num_vt * prm.B;
+  if (cta_group == 2) return launch_fwd_impl<2>(tmE, tmH, prm, num_sms, stream);
+  return launch_fwd_impl<1>(tmE, tmH, prm, num_sms, stream);
+}
+
+int fwd_smem_bytes(int cta_group) {
+  return cta_group == 2 ? FwdCfg<2>::SMEM_BYTES : FwdCfg<1>::SMEM_BYTES;
+}
+
+}  // namespace sparton

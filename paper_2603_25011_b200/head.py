@@ -1,0 +1,194 @@
+"""Torch-facing Sparton head: functional forward/backward and the autograd.Function.
+
+The reference has no torch API; this is the GPU-native form of
+its operator pair ``forward_fully_fused`` / ``backward_fused``
+(/root/reference/pkg/src/fusedhead/fused.py:160-212, :215-278).  Torch is
+plumbing here: it owns device memory (caching allocator, so peak-HBM numbers
+stay in torch's accounting) and streams; every byte of arithmetic runs in the
+sm_100a kernels behind the C ABI (``_lib``).  There is no CPU path: non-CUDA
+tensors raise.
+
+State kept for backward is exactly (Y, I) — B·V·(4+4) bytes, independent of S —
+plus references to the inputs H and E (SavedSparseState, fused.py:67-80).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+__all__ = [
+    "sparton_forward",
+    "sparton_backward",
+    "SpartonHeadFn",
+    "sparton_head",
+    "bwd_workspace_bytes",
+]
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _require_cuda(name: str, t: torch.Tensor) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise RuntimeError(
+            f"{name} is on {t.device}: the sparton head runs only on CUDA (sm_100a); there is no CPU fallback")
+
+
+def _pad_hidden(x: torch.Tensor) -> torch.Tensor:
+    """Zero-pad the hidden axis to a multiple of 8 (TMA stride rule); zero K
+    columns add exactly 0 to every dot product."""
+    d = x.shape[-1]
+    if d % 8 == 0:
+        return x
+    return torch.nn.functional.pad(x, (0, 8 - d % 8))
+
+
+def _check_inputs(H, E, bias, mask):
+    for name, t in (("H", H), ("E", E), ("bias", bias), ("mask", mask)):
+        _require_cuda(name, t)
+    if H.dim() != 3:
+        raise ValueError(f"H must be (B, S, D), got shape {tuple(H.shape)}")
+    B, S, D = H.shape
+    if E.dim() != 2 or E.shape[1] != D:
+        raise ValueError(f"E must be (V, {D}), got shape {tuple(E.shape)}")
+    V = E.shape[0]
+    if H.dtype != torch.bfloat16 or E.dtype != torch.bfloat16:
+        raise ValueError(f"H and E must be bfloat16, got {H.dtype} and {E.dtype}")
+    if bias.shape != (V,) or bias.dtype != torch.float32:
+        raise ValueError(f"bias must be float32 of shape ({V},), got {bias.dtype} {tuple(bias.shape)}")
+    if mask.shape != (B, S) or mask.dtype not in (torch.uint8, torch.bool):
+        raise ValueError(f"mask must be uint8/bool of shape ({B}, {S}), got {mask.dtype} {tuple(mask.shape)}")
+    if min(B, S, D, V) < 1:
+        raise ValueError(f"all dims must be positive, got B={B} S={S} D={D} V={V}")
+    return B, S, D, V
+
+
+@torch.no_grad()
+def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,
+                    *, cta_group: int = 0, out: tuple[torch.Tensor, torch.Tensor] | None = None
+                    ) -> tuple[torch.Tensor, torch.Tensor]:
+    """Fused head forward: returns (Y f32 [B, V], I int32 [B, V]).
+
+    Y[b,v] = log1p(relu(max_s((H[b,s]·E[v] + bias[v]) · mask[b,s]))), I = first argmax.
+    The B×S×V logits are never materialised.
+    """
+    B, S, D, V = _check_inputs(H, E, bias, mask)
+    Hp = _pad_hidden(H.contiguous()).reshape(B * S, -1)
+    Ep = _pad_hidden(E.contiguous())
+    Dp = Hp.shape[1]
+    m = mask.contiguous()
+    if m.dtype == torch.bool:
+        m = m.view(torch.uint8)
+    bias = bias.contiguous()
+    if out is None:
+        Y = torch.empty((B, V), dtype=torch.float32, device=H.device)
+        I = torch.empty((B, V), dtype=torch.int32, device=H.device)
+    else:
+        Y, I = out
+        if Y.shape != (B, V) or I.shape != (B, V) or Y.dtype != torch.float32 or I.dtype != torch.int32:
+            raise ValueError("out must be (Y float32 [B,V], I int32 [B,V])")
+    ldY = Y.stride(0)
+    if Y.stride(1) != 1 or I.stride(1) != 1 or I.stride(0) != ldY:
+        raise ValueError("Y and I must share a row stride with unit column stride")
+    lib = _lib.load()
+    with torch.cuda.device(H.device):
+        rc = lib.sparton_fwd(Hp.data_ptr(), Ep.data_ptr(), bias.data_ptr(), m.data_ptr(),
+                             Y.data_ptr(), I.data_ptr(), B, S, Dp, V, ldY, int(cta_group), _stream_ptr())
+    _lib.check(rc)
+    return Y, I
+
+
+def bwd_workspace_bytes(B: int, S: int, V: int) -> int:
+    return int(_lib.load().sparton_bwd_workspace_bytes(B, S, V))
+
+
+@torch.no_grad()
+def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch.Tensor,
+                     dY: torch.Tensor, *, include_bias_grad: bool = True,
+                     grad_dtype: torch.dtype = torch.float32
+                     ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Argmax-routed backward from the saved (Y, I) only (fused.py:215-278).
+
+    Returns (dH [B,S,D], dE [V,D], db [V] f32); dH/dE in ``grad_dtype``
+    (float32 or bfloat16), accumulated in fp32 by single-owner kernels.
+    Like the reference, only shapes are validated (fused.py:232-245).
+    """
+    for name, t in (("H", H), ("E", E), ("Y", Y), ("I", I), ("dY", dY)):
+        _require_cuda(name, t)
+    if H.dim() != 3 or E.dim() != 2 or E.shape[1] != H.shape[2]:
+        raise ValueError("input shapes disagree with dims")
+    B, S, D = H.shape
+    V = E.shape[0]
+    if Y.shape != (B, V) or I.shape != (B, V):
+        raise ValueError(f"saved state must have shape {(B, V)}")
+    if dY.shape != (B, V):
+        raise ValueError(f"dY must have shape {(B, V)}, got {tuple(dY.shape)}")
+    if Y.dtype != torch.float32 or I.dtype != torch.int32 or dY.dtype != torch.float32:
+        raise ValueError("Y/dY must be float32 and I int32")
+    if grad_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("grad_dtype must be torch.float32 or torch.bfloat16")
+    Hp = _pad_hidden(H.contiguous())
+    Ep = _pad_hidden(E.contiguous())
+    Dp = Hp.shape[2]
+    Y = Y.contiguous()
+    I = I.contiguous()
+    dY = dY.contiguous()
+    dev = H.device
+    dH = torch.empty((B, S, Dp), dtype=grad_dtype, device=dev)
+    dE = torch.empty((V, Dp), dtype=grad_dtype, device=dev)
+    db = torch.empty((V,), dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    ws_bytes = int(lib.sparton_bwd_workspace_bytes(B, S, V))
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+    gd = _lib.SPARTON_BF16 if grad_dtype == torch.bfloat16 else _lib.SPARTON_F32
+    with torch.cuda.device(dev):
+        rc = lib.sparton_bwd(Hp.data_ptr(), Ep.data_ptr(), Y.data_ptr(), I.data_ptr(), dY.data_ptr(),
+                             dH.data_ptr(), dE.data_ptr(), db.data_ptr(), B, S, Dp, V, Y.stride(0),
+                             dY.stride(0), int(bool(include_bias_grad)), gd, ws.data_ptr(), ws_bytes,
+                             _stream_ptr())
+    _lib.check(rc)
+    if Dp != D:
+        dH = dH[..., :D]
+        dE = dE[:, :D]
+    return dH, dE, db
+
+
+class SpartonHeadFn(torch.autograd.Function):
+    """Autograd op: Y = SpartonHead(H, E, bias, mask).
+
+    forward saves (H, E, Y, I) — H and E are the caller's tensors, so the head
+    adds only B·V·8 bytes of saved state (SavedSparseState, fused.py:67-80).
+    backward returns (dH, dE, db, None) in the input dtypes.
+    """
+
+    @staticmethod
+    def forward(ctx, H, E, bias, mask, include_bias_grad=True):
+        Y, I = sparton_forward(H, E, bias, mask)
+        ctx.save_for_backward(H, E, Y, I)
+        ctx.include_bias_grad = bool(include_bias_grad)
+        ctx.mark_non_differentiable(I)
+        return Y, I
+
+    @staticmethod
+    def backward(ctx, dY, dI_unused):
+        H, E, Y, I = ctx.saved_tensors
+        if dY is None:
+            return None, None, None, None, None
+        dH, dE, db = sparton_backward(H, E, Y, I, dY.float(), include_bias_grad=ctx.include_bias_grad,
+                                      grad_dtype=H.dtype)
+        if dE.dtype != E.dtype:
+            dE = dE.to(E.dtype)
+        return dH, dE, db, None, None
+
+
+def sparton_head(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,
+                 *, return_indices: bool = False, include_bias_grad: bool = True):
+    """Differentiable SPLADE max-pooled LM head (drop-in for the naive
+    ``((H@E.T + b) * M[...,None]).relu().log1p().max(dim=1)``)."""
+    Y, I = SpartonHeadFn.apply(H, E, bias, mask, include_bias_grad)
+    return (Y, I) if return_indices else Y

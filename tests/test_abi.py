@@ -1,0 +1,89 @@
+"""The C-ABI library loads and exports exactly what include/sparton.h declares.
+
+CPU-only: no kernel is launched.  Argument validation happens before any CUDA
+call, so EINVAL paths are exercised here too.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+
+import pytest
+
+from conftest import REPO
+
+
+def _declared():
+    hdr = (REPO / "include" / "sparton.h").read_text()
+    return sorted(set(re.findall(r"SPARTON_API\s+[\w\s\*]+?\b(sparton_\w+)\s*\(", hdr)))
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    assert names == sorted(["sparton_abi_version", "sparton_last_error", "sparton_device_sm_count",
+                            "sparton_fwd", "sparton_bwd_workspace_bytes", "sparton_bwd"])
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert set(_lib.EXPORTED) == set(_declared())
+    assert lib.sparton_abi_version() == 100
+
+
+def test_workspace_formula():
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    B, S, V = 512, 512, 250002
+    pairs = (B * V * 8 + 255) // 256 * 256
+    offs = (B * (S + 1) * 4 + 255) // 256 * 256
+    assert lib.sparton_bwd_workspace_bytes(B, S, V) == pairs + offs
+    assert lib.sparton_bwd_workspace_bytes(0, S, V) == 0
+
+
+@pytest.mark.parametrize("dims", [(0, 3, 8, 5), (2, 3, 4, 5), (2, -1, 8, 5)])
+def test_fwd_rejects_bad_dims_before_any_cuda_call(dims):
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    B, S, D, V = dims
+    dummy = ctypes.c_void_p(16)
+    rc = lib.sparton_fwd(dummy, dummy, dummy, dummy, dummy, dummy, B, S, D, V, V, 0, None)
+    assert rc == _lib.SPARTON_EINVAL
+    assert lib.sparton_last_error()
+    with pytest.raises(ValueError):
+        _lib.check(rc)
+
+
+def test_fwd_rejects_null_and_misaligned():
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    a = ctypes.c_void_p(256)
+    assert lib.sparton_fwd(None, a, a, a, a, a, 2, 3, 8, 5, 5, 0, None) == _lib.SPARTON_EINVAL
+    odd = ctypes.c_void_p(258)
+    assert lib.sparton_fwd(odd, a, a, a, a, a, 2, 3, 8, 5, 5, 0, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_fwd(a, a, a, a, a, a, 2, 3, 8, 5, 4, 0, None) == _lib.SPARTON_EINVAL  # ldY < V
+    assert lib.sparton_fwd(a, a, a, a, a, a, 2, 3, 8, 5, 5, 3, None) == _lib.SPARTON_EINVAL  # cta_group
+
+
+def test_bwd_rejects_small_workspace():
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    a = ctypes.c_void_p(256)
+    rc = lib.sparton_bwd(a, a, a, a, a, a, a, a, 2, 3, 8, 5, 5, 5, 1, 0, a, 16, None)
+    assert rc == _lib.SPARTON_EINVAL
+    assert b"workspace" in lib.sparton_last_error()
+    rc = lib.sparton_bwd(a, a, a, a, a, a, a, a, 2, 3, 8, 5, 5, 5, 1, 7, a, 1 << 20, None)
+    assert rc == _lib.SPARTON_EINVAL
+
+
+def test_sm_count_query_is_safe_without_gpu():
+    from paper_2603_25011_b200 import _lib
+    import torch
+    n = _lib.load().sparton_device_sm_count()
+    if not torch.cuda.is_available():
+        assert n == 0
+    else:
+        assert n > 0
