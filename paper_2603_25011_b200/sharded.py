@@ -1,0 +1,122 @@
+"""Vocab-sharded (column-parallel) Sparton head over torch.distributed / NCCL.
+
+Each output column v depends only on E[v] and b[v], so rank p
+owns vocab rows [p·Vp, min((p+1)·Vp, V)) with Vp = ⌈V/P⌉ and runs the fused
+forward on its shard with no communication; the B×V output is assembled by
+one all-gather of the (Y, I) shards.  The backward is local for dE/db; dH is a
+sum over every rank's vocab shard, so the per-rank partial dH (fp32) is
+all-reduced.  H, mask and dY are replicated (dY columns are sliced in place).
+
+The local compute is injectable (``local_fn`` / ``local_bwd``) so the sharding
+and assembly logic is tested on CPU with the gloo backend; on GPU it is the
+sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .head import sparton_backward, sparton_forward
+
+
+def shard_range(V: int, world: int, rank: int) -> tuple[int, int, int]:
+    """(v0, v1, Vp): this rank's vocab rows [v0, v1) and the padded shard width."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world {world}")
+    Vp = (V + world - 1) // world
+    v0 = min(V, rank * Vp)
+    v1 = min(V, (rank + 1) * Vp)
+    return v0, v1, Vp
+
+
+def _world(group):
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def local_forward(H, E_shard, bias_shard, mask, out=None):
+    """K1 on this rank's vocab shard."""
+    return sparton_forward(H, E_shard, bias_shard, mask, out=out)
+
+
+def gather_vocab(Y_p: torch.Tensor, I_p: torch.Tensor, V: int, Vp: int, group=None):
+    """All-gather the per-rank (Y, I) column shards into full [B, V] tensors.
+
+    Shards are padded to Vp columns (NCCL needs equal counts); the padding sits
+    only at the tail of the last shard(s), so concatenating shards in rank
+    order and cutting at V is exact."""
+    world, _ = _world(group)
+    B, n = Y_p.shape
+    if world == 1:
+        return Y_p, I_p
+    Yb = torch.zeros((B, Vp), dtype=Y_p.dtype, device=Y_p.device)
+    Ib = torch.zeros((B, Vp), dtype=I_p.dtype, device=I_p.device)
+    Yb[:, :n] = Y_p
+    Ib[:, :n] = I_p
+    ys = [torch.empty_like(Yb) for _ in range(world)]
+    is_ = [torch.empty_like(Ib) for _ in range(world)]
+    dist.all_gather(ys, Yb, group=group)
+    dist.all_gather(is_, Ib, group=group)
+    Y = torch.cat(ys, dim=1)[:, :V].contiguous()
+    I = torch.cat(is_, dim=1)[:, :V].contiguous()
+    return Y, I
+
+
+def local_backward(H, E_shard, Y_p, I_p, dY_p, *, grad_dtype=torch.float32, include_bias_grad=True,
+                   group=None, local_bwd: Callable | None = None):
+    """Shard-local K2/K3 then an all-reduce of the partial dH (fp32)."""
+    fn = local_bwd or sparton_backward
+    dH, dE, db = fn(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
+                    grad_dtype=torch.float32)
+    world, _ = _world(group)
+    if world > 1:
+        dist.all_reduce(dH, op=dist.ReduceOp.SUM, group=group)
+    if grad_dtype != torch.float32:
+        dH = dH.to(grad_dtype)
+        dE = dE.to(grad_dtype)
+    return dH, dE, db
+
+
+def forward_sharded(H, E_shard, bias_shard, mask, V: int, *, group=None,
+                    local_fn: Callable | None = None):
+    """Full (Y, I) [B, V] from this rank's vocab shard of E/bias."""
+    world, rank = _world(group)
+    v0, v1, Vp = shard_range(V, world, rank)
+    if E_shard.shape[0] != v1 - v0:
+        raise ValueError(f"rank {rank} expects {v1 - v0} vocab rows, got {E_shard.shape[0]}")
+    B = H.shape[0]
+    fn = local_fn or local_forward
+    if v1 > v0:
+        Y_p, I_p = fn(H, E_shard, bias_shard, mask)
+    else:
+        Y_p = torch.zeros((B, 0), dtype=torch.float32, device=H.device)
+        I_p = torch.zeros((B, 0), dtype=torch.int32, device=H.device)
+    return gather_vocab(Y_p, I_p, V, Vp, group=group)
+
+
+class ShardedSpartonHeadFn(torch.autograd.Function):
+    """Autograd op for the vocab-sharded head: returns the full Y [B, V];
+    gradients: dH (all-reduced), dE/db for this rank's shard only."""
+
+    @staticmethod
+    def forward(ctx, H, E_shard, bias_shard, mask, V, group=None):
+        world, rank = _world(group)
+        v0, v1, Vp = shard_range(V, world, rank)
+        Y_p, I_p = local_forward(H, E_shard, bias_shard, mask)
+        ctx.save_for_backward(H, E_shard, Y_p, I_p)
+        ctx.v = (v0, v1)
+        ctx.group = group
+        Y, _ = gather_vocab(Y_p, I_p, V, Vp, group=group)
+        return Y
+
+    @staticmethod
+    def backward(ctx, dY):
+        H, E_shard, Y_p, I_p = ctx.saved_tensors
+        v0, v1 = ctx.v
+        dH, dE, db = local_backward(H, E_shard, Y_p, I_p, dY[:, v0:v1].contiguous().float(),
+                                    grad_dtype=H.dtype, group=ctx.group)
+        return dH, dE.to(E_shard.dtype), db, None, None, None
