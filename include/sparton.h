@@ -80,9 +80,12 @@ SPARTON_API int sparton_fwd(const void* H, const void* E, const float* bias, con
                 int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY,
                 int cta_group, void* stream);
 
-/* Workspace bytes sparton_bwd needs for these sizes (argmax-routed pair lists
- * for dH: B*V*8 bytes + offsets).  Pure host arithmetic. */
-SPARTON_API size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t V);
+/* Workspace bytes sparton_bwd needs for these sizes: the argmax-routed (v, g)
+ * pair lists for dH (B*V*8 bytes), their offsets and per-row cursors, plus an
+ * fp32 dH accumulator (B*S*D*4) when grad_dtype is bf16 and the vocabulary is
+ * processed in more than one L2-sized chunk.  Pure host arithmetic. */
+SPARTON_API size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t D, int64_t V,
+                                               int grad_dtype);
 
 /*
  * Backward.  Replaces backward_fused (fused.py:215-278) from the saved
@@ -92,7 +95,7 @@ SPARTON_API size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t V);
  * element has a single owner that accumulates in the reference's order.
  *   dY : f32 [B, ldDY]    dH : [B*S, D]   dE : [V, D]   db : f32 [V]
  *   grad_dtype : SPARTON_F32 or SPARTON_BF16 for dH and dE.
- *   workspace  : >= sparton_bwd_workspace_bytes(B, S, V) bytes, 16-B aligned.
+ *   workspace  : >= sparton_bwd_workspace_bytes(B, S, D, V, grad_dtype) bytes, 16-B aligned.
  */
 SPARTON_API int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I,
                 const float* dY, void* dH, void* dE, float* db,

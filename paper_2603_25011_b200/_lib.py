@@ -65,7 +65,7 @@ def load() -> ctypes.CDLL:
         lib.sparton_fwd.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                     c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]
         lib.sparton_bwd_workspace_bytes.restype = ctypes.c_size_t
-        lib.sparton_bwd_workspace_bytes.argtypes = [c_i64, c_i64, c_i64]
+        lib.sparton_bwd_workspace_bytes.argtypes = [c_i64, c_i64, c_i64, c_i64, c_int]
         lib.sparton_bwd.restype = c_int
         lib.sparton_bwd.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                     c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,

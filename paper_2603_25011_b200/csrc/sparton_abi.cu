@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "sparton_internal.h"
@@ -175,12 +176,16 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
   prm.D = (int)D;
   prm.V = (int)V;
   prm.ldY = ldY;
+  {
+    const char* ev = getenv("SPARTON_E_EVICT_LAST");
+    prm.e_evict_last = (ev && ev[0] == '0') ? 0 : 1;
+  }
   return launch_fwd(tmE, tmH, prm, cg, d.sms, static_cast<cudaStream_t>(stream));
 }
 
-size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t V) {
-  if (B < 1 || S < 1 || V < 1) return 0;
-  return bwd_workspace_bytes(B, S, V);
+size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t D, int64_t V, int grad_dtype) {
+  if (B < 1 || S < 1 || D < 1 || V < 1) return 0;
+  return bwd_workspace_layout(B, S, D, V, grad_dtype).total;
 }
 
 int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, const float* dY,
@@ -197,7 +202,8 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
   if (grad_dtype != SPARTON_F32 && grad_dtype != SPARTON_BF16)
     return set_error(SPARTON_EINVAL, "grad_dtype must be SPARTON_F32 or SPARTON_BF16");
   if (S > bwd_max_seq()) return set_error(SPARTON_EINVAL, "S exceeds the backward's routing limit");
-  const size_t need = bwd_workspace_bytes(B, S, V);
+  const BwdWorkspace ws = bwd_workspace_layout(B, S, D, V, grad_dtype);
+  const size_t need = ws.total;
   if (workspace_bytes < need) {
     char buf[160];
     snprintf(buf, sizeof(buf), "workspace too small: %zu < %zu bytes", workspace_bytes, need);
@@ -220,9 +226,20 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
   p.ldY = ldY;
   p.ldDY = ldDY;
   p.include_bias_grad = include_bias_grad;
-  const size_t pairs_bytes = ((size_t)B * (size_t)V * sizeof(int2) + 255) & ~size_t(255);
-  p.pairs = static_cast<int2*>(workspace);
-  p.offsets = reinterpret_cast<int*>(static_cast<char*>(workspace) + pairs_bytes);
+  char* wsb = static_cast<char*>(workspace);
+  p.pairs = reinterpret_cast<int2*>(wsb + ws.pairs);
+  p.offsets = reinterpret_cast<int*>(wsb + ws.offsets);
+  p.acc32 = ws.acc32 == (size_t)-1 ? nullptr : reinterpret_cast<float*>(wsb + ws.acc32);
+  p.dE_acc = ws.dE_acc == (size_t)-1 ? nullptr : reinterpret_cast<float*>(wsb + ws.dE_acc);
+  p.db_acc = reinterpret_cast<float*>(wsb + ws.db_acc);
+  p.bchunk = ws.bchunk;
+  {
+    const char* ev = getenv("SPARTON_DE_STAGGER");
+    p.de_stagger = (ev && ev[0] == '1') ? 1 : 0;
+  }
+  p.nwin = ws.nwin;
+  p.wpc = ws.wpc;
+  p.nchunks = ws.nchunks;
   return launch_bwd(p, grad_dtype, static_cast<cudaStream_t>(stream));
 }
 

@@ -12,15 +12,17 @@
 // reference's order — b ascending for dE/db, v ascending for dH.
 //
 //   K2 sparton_bwd_de_kernel  : CTA owns 32 vocab rows x one D slice; warps own
-//                               4 rows each, lanes own 8-wide D chunks; (g, I)
-//                               tiles for 32 batch rows are staged in smem and
-//                               the H rows at the argmax are gathered (16-B
-//                               vector loads, 4 rows in flight per warp).
-//   K3a sparton_bwd_route_kernel : CTA per batch row: a stable counting sort of
-//                               the active (v, g) pairs by argmax position s,
-//                               giving per-(b,s) lists in ascending v.
+//                               4 vocab rows, lanes 8-wide D chunks; for each
+//                               batch row (ascending) each warp gathers its
+//                               argmax H rows with 1-D TMA bulk copies into a
+//                               private mbarrier ring, 4 batch rows deep.
+//   K3a sparton_bwd_route_kernel : CTA per (vocab window, b): a stable counting
+//                               sort in smem of the window's active (v, g) pairs
+//                               by argmax position s, written out coalesced as
+//                               per-(b, window, s) lists in ascending v.
 //   K3b sparton_bwd_dh_kernel : warp owns one (b, s) row (x D slice) and sums
-//                               g * E[v,:] over its list in ascending v.
+//                               g * E[v,:] over its list in ascending v, in
+//                               L2-sized vocabulary chunks (one launch each).
 // All arithmetic is fp32 (inputs bf16), exactly one owner per output element.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -35,24 +37,40 @@ namespace sparton {
 namespace {
 
 constexpr int DE_VB = 32;       // vocab rows per CTA
-constexpr int DE_BC = 32;       // batch rows staged per smem tile
-constexpr int DE_THREADS = 256; // 8 warps x 4 vocab rows
-constexpr int ROUTE_THREADS = 1024;
-constexpr int ROUTE_SMEM_INTS = 48 * 1024;  // per-warp histograms (192 KB)
+constexpr int DE_RPW = 2;       // vocab rows per warp
+constexpr int DE_WARPS = DE_VB / DE_RPW;
+constexpr int DE_THREADS = DE_WARPS * 32;
 constexpr int DH_THREADS = 256;
+constexpr int DH_UNROLL = 4;   // E rows in flight per warp
 
 __device__ __forceinline__ float pair_grad(float y, float dy) {
   // exp(-Y) == 1/(1+rawmax) (fused.py:247-249); accurate expf, no fast-math.
   return dy * expf(-y);
 }
 
-__device__ __forceinline__ void fma8(float* acc, float g, const int4& raw) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+// acc[0..7] += g * bf16x8(raw), as four packed fp32x2 FMAs (FFMA2: two
+// independent round-to-nearest fp32 FMAs, bit-identical to scalar fmaf).
+// bf16 -> fp32 is exact: the low half of each 32-bit word moves to the top
+// (shl 16), the high half is masked in place.
+__device__ __forceinline__ uint64_t pack_gg(float g) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(g));
+  return r;
+}
+
+__device__ __forceinline__ void fma8(float* acc, uint64_t gg, const int4& raw) {
+  const uint32_t w[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float2 f = __bfloat1622float2(h[i]);
-    acc[2 * i] = fmaf(g, f.x, acc[2 * i]);
-    acc[2 * i + 1] = fmaf(g, f.y, acc[2 * i + 1]);
+    asm("{\n.reg .b32 lo, hi;\n.reg .b64 x, a;\n"
+        "shl.b32 lo, %2, 16;\n"
+        "and.b32 hi, %2, 0xffff0000;\n"
+        "mov.b64 x, {lo, hi};\n"
+        "mov.b64 a, {%0, %1};\n"
+        "fma.rn.f32x2 a, x, %3, a;\n"
+        "mov.b64 {%0, %1}, a;\n}\n"
+        : "+f"(acc[2 * i]), "+f"(acc[2 * i + 1])
+        : "r"(w[i]), "l"(gg));
   }
 }
 
@@ -75,133 +93,254 @@ __device__ __forceinline__ void store8<__nv_bfloat16>(__nv_bfloat16* dst, const 
 }
 
 // ------------------------------------------------------------------ K2: dE, db
+// CTA = 32 vocab rows x one D slice (DS = 256*CPL columns); 16 warps own 2
+// vocab rows each, lanes own 8-wide D chunks, fp32 accumulators in registers.
+// Batch rows are visited in ascending order (the reference's order).  Each
+// warp runs its own NST-deep TMA pipeline: lanes 0..1 gather the warp's 2
+// argmax H rows H[b, I[b,v], slice] for batch row b+NST-1 with 1-D bulk copies
+// (cp.async.bulk, one instruction per row) into a private smem ring, lane 0
+// arms that stage's mbarrier with the byte count; the warp consumes stage b.
+// No register staging and no CTA-wide barrier on the gather path, so ~144 KB
+// of rows are in flight per SM.  (g, I) for 32 batch rows at a time are
+// staged in smem (double buffered, one __syncthreads per 32 batch rows).
+constexpr int DE_BC = 32;       // batch rows per (g, I) tile
+
+template <int CPL>
+struct DeCfg {
+  static constexpr int DS = 256 * CPL;                       // slice width (elements)
+  static constexpr int ROW_BYTES = DS * 2;
+  static constexpr int NST = CPL >= 3 ? 4 : (CPL == 2 ? 6 : 8);
+  static constexpr int WARP_STAGE_BYTES = DE_RPW * ROW_BYTES;  // DE_RPW rows per warp per stage
+  static constexpr int RING_BYTES = DE_WARPS * NST * WARP_STAGE_BYTES;
+  static constexpr int GI_BYTES = 2 * 2 * DE_BC * DE_VB * 4;  // g and I, double buffered
+  static constexpr int BAR_BYTES = DE_WARPS * NST * 8;
+  static constexpr int SMEM_BYTES = RING_BYTES + GI_BYTES + BAR_BYTES;
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
 template <int CPL, typename OutT>
-__global__ void __launch_bounds__(DE_THREADS)
-sparton_bwd_de_kernel(const BwdParams p) {
-  __shared__ float g_s[DE_BC][DE_VB];
-  __shared__ int i_s[DE_BC][DE_VB];
+__global__ void __launch_bounds__(DE_THREADS, 1)
+sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
+  using C = DeCfg<CPL>;
+  extern __shared__ __align__(128) uint8_t de_smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  uint8_t* ring = de_smem + (size_t)warp * C::NST * C::WARP_STAGE_BYTES;       // this warp's ring
+  float* g_s = reinterpret_cast<float*>(de_smem + C::RING_BYTES);               // [2][BC][VB]
+  int* i_s = reinterpret_cast<int*>(g_s + 2 * DE_BC * DE_VB);                   // [2][BC][VB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(de_smem + C::RING_BYTES + C::GI_BYTES) + warp * C::NST;
+
   const int v0 = blockIdx.x * DE_VB;
-  const int d0 = blockIdx.y * (256 * CPL);
+  const int d0 = blockIdx.y * C::DS;
+  const uint32_t slice_bytes = (uint32_t)min(C::DS, p.D - d0) * 2u;
+  const int nb = bend - bbeg;                // batch rows of this pass (local index lb = b - bbeg)
+  const int rot = p.de_stagger ? (int)(blockIdx.x % (unsigned)nb) : 0;   // experiment: rotated start
+  const bool first = bbeg == 0;
+  const bool last = bend == p.B;
 
-  float acc[4][CPL * 8];
-  float gsum[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    gsum[r] = 0.f;
-#pragma unroll
-    for (int i = 0; i < CPL * 8; ++i) acc[r][i] = 0.f;
+  if (lane == 0) {
+    for (int i = 0; i < C::NST; ++i) ptx::mbar_init(ptx::smem_u32(&bars[i]), 1);
+    ptx::fence_mbar_init();
   }
-  bool dvalid[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) dvalid[c] = (d0 + c * 256 + lane * 8) < p.D;
 
-  for (int b0 = 0; b0 < p.B; b0 += DE_BC) {
-    // Stage g and I for DE_BC batch rows x DE_VB vocab rows (coalesced rows of 128 B).
+  // Stage g and I of local batch rows [lb0, lb0 + DE_BC) into buffer `buf`.
+  auto stage_gi = [&](int lb0, int buf) {
     for (int e = threadIdx.x; e < DE_BC * DE_VB; e += DE_THREADS) {
       const int bb = e / DE_VB, vv = e % DE_VB;
-      const int b = b0 + bb, v = v0 + vv;
+      const int lq = lb0 + bb, v = v0 + vv;
       float g = 0.f;
       int idx = -1;
-      if (b < p.B && v < p.V) {
-        const float y = p.Y[(size_t)b * p.ldY + v];
+      if (lq < nb && v < p.V) {
+        const int lb = lq + rot < nb ? lq + rot : lq + rot - nb;
+        const size_t b = (size_t)(bbeg + lb);
+        const float y = p.Y[b * p.ldY + v];
         if (y > 0.f) {
-          g = pair_grad(y, p.dY[(size_t)b * p.ldDY + v]);
-          idx = p.I[(size_t)b * p.ldY + v];
+          g = pair_grad(y, p.dY[b * p.ldDY + v]);
+          idx = p.I[b * p.ldY + v];
         }
       }
-      g_s[bb][vv] = g;
-      i_s[bb][vv] = idx;
+      g_s[(buf * DE_BC + bb) * DE_VB + vv] = g;
+      i_s[(buf * DE_BC + bb) * DE_VB + vv] = idx;
     }
-    __syncthreads();
-    const int nb = min(DE_BC, p.B - b0);
-    for (int bb = 0; bb < nb; ++bb) {
-      const size_t hbase = (size_t)(b0 + bb) * p.S;
-      int4 raw[4][CPL];
-      float g[4];
-      bool act[4];
+  };
+  // Lanes 0..DE_RPW-1 gather this warp's rows for local batch row lb into ring stage
+  // lb % NST (one bulk copy each); lane 0 arms the stage barrier with the total.
+  auto issue = [&](int lb) {
+    const int t = lb / DE_BC, bb = lb - t * DE_BC, buf = t & 1;
+    const int st = lb % C::NST;
+    const uint32_t bar = ptx::smem_u32(&bars[st]);
+    const int idx = lane < DE_RPW ? i_s[(buf * DE_BC + bb) * DE_VB + warp + DE_WARPS * lane] : -1;
+    const unsigned act = __ballot_sync(0xffffffffu, idx >= 0);
+    if (lane == 0) ptx::mbar_arrive_expect_tx(bar, (uint32_t)__popc(act) * slice_bytes);
+    if (idx >= 0) {
+      const int lbr = lb + rot < nb ? lb + rot : lb + rot - nb;
+      const size_t hrow = (size_t)(bbeg + lbr) * p.S + idx;
+      bulk_g2s(ptx::smem_u32(ring + st * C::WARP_STAGE_BYTES + lane * C::ROW_BYTES),
+               p.H + hrow * (size_t)p.D + d0, slice_bytes, bar);
+    }
+  };
+
+  float acc[DE_RPW][CPL * 8];
+  float gsum[DE_RPW];
+  bool dvalid[CPL];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int vv = warp + 8 * r;
-        const int idx = i_s[bb][vv];
-        g[r] = g_s[bb][vv];
-        act[r] = idx >= 0;
-        const __nv_bfloat16* row = p.H + (hbase + (act[r] ? idx : 0)) * (size_t)p.D + d0 + lane * 8;
+  for (int c = 0; c < CPL; ++c) dvalid[c] = (c * 256 + lane * 8) * 2 < (int)slice_bytes;
+  // fp32 carry from the previous pass (the fp32 output itself, or the workspace).
+  float* carry = p.dE_acc ? p.dE_acc : reinterpret_cast<float*>(p.dE);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          raw[r][c] = (act[r] && dvalid[c]) ? __ldg(reinterpret_cast<const int4*>(row + c * 256))
-                                           : make_int4(0, 0, 0, 0);
+  for (int r = 0; r < DE_RPW; ++r) {
+    const int v = v0 + warp + DE_WARPS * r;
+    gsum[r] = (!first && v < p.V) ? p.db_acc[v] : 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      if (!first && v < p.V && dvalid[c]) {
+        const float* src = carry + (size_t)v * p.D + d0 + c * 256 + lane * 8;
+        const float4 a = *reinterpret_cast<const float4*>(src);
+        const float4 bq = *reinterpret_cast<const float4*>(src + 4);
+        acc[r][c * 8 + 0] = a.x; acc[r][c * 8 + 1] = a.y; acc[r][c * 8 + 2] = a.z; acc[r][c * 8 + 3] = a.w;
+        acc[r][c * 8 + 4] = bq.x; acc[r][c * 8 + 5] = bq.y; acc[r][c * 8 + 6] = bq.z; acc[r][c * 8 + 7] = bq.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[r][c * 8 + i] = 0.f;
       }
+    }
+  }
+
+  const int ntiles = (nb + DE_BC - 1) / DE_BC;
+  stage_gi(0, 0);
+  if (ntiles > 1) stage_gi(DE_BC, 1);
+  __syncthreads();
+  // Prologue: NST-1 batch rows in flight (all within tiles 0/1, NST-1 < DE_BC).
+  for (int lb = 0; lb < C::NST - 1 && lb < nb; ++lb) issue(lb);
+  uint32_t phase_bits = 0;   // parity per stage
+
+  for (int lb = 0; lb < nb; ++lb) {
+    const int t = lb / DE_BC, bb = lb - t * DE_BC, buf = t & 1;
+    if (bb == 0 && t > 0) {
+      // Tile t is resident (staged one tile ahead); refill the other buffer with
+      // tile t+1 once every warp is done with tile t-1.
+      __syncthreads();
+      if (t + 1 < ntiles) stage_gi((t + 1) * DE_BC, buf ^ 1);
+      __syncthreads();
+    }
+    // Issue local batch row lb+NST-1: its tile is t or t+1 (NST-1 < DE_BC), both resident.
+    if (lb + C::NST - 1 < nb) {
+      ptx::fence_proxy_async();
+      issue(lb + C::NST - 1);
+    }
+    const int st = lb % C::NST;
+    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (phase_bits >> st) & 1u);
+    phase_bits ^= 1u << st;
+    const uint8_t* src = ring + st * C::WARP_STAGE_BYTES;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (act[r]) {
-          gsum[r] += g[r];
+    for (int r = 0; r < DE_RPW; ++r) {
+      const int vv = warp + DE_WARPS * r;
+      const int idx = i_s[(buf * DE_BC + bb) * DE_VB + vv];
+      if (idx >= 0) {
+        const float g = g_s[(buf * DE_BC + bb) * DE_VB + vv];
+        gsum[r] += g;
+        const uint64_t gg = pack_gg(g);
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) fma8(&acc[r][c * 8], g[r], raw[r][c]);
+        for (int c = 0; c < CPL; ++c) {
+          if (dvalid[c]) {
+            const int4 x = *reinterpret_cast<const int4*>(src + r * C::ROW_BYTES + (c * 256 + lane * 8) * 2);
+            fma8(&acc[r][c * 8], gg, x);
+          }
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
 
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int v = v0 + warp + 8 * r;
+  for (int r = 0; r < DE_RPW; ++r) {
+    const int v = v0 + warp + DE_WARPS * r;
     if (v >= p.V) continue;
-    OutT* dst = reinterpret_cast<OutT*>(p.dE) + (size_t)v * p.D + d0 + lane * 8;
+    if (last) {
+      OutT* dst = reinterpret_cast<OutT*>(p.dE) + (size_t)v * p.D + d0 + lane * 8;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c)
-      if (dvalid[c]) store8<OutT>(dst + c * 256, &acc[r][c * 8]);
-    if (blockIdx.y == 0 && lane == 0 && p.db != nullptr)
-      p.db[v] = p.include_bias_grad ? gsum[r] : 0.f;
+      for (int c = 0; c < CPL; ++c)
+        if (dvalid[c]) store8<OutT>(dst + c * 256, &acc[r][c * 8]);
+      if (blockIdx.y == 0 && lane == 0 && p.db != nullptr)
+        p.db[v] = p.include_bias_grad ? gsum[r] : 0.f;
+    } else {
+      float* dst = carry + (size_t)v * p.D + d0 + lane * 8;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        if (dvalid[c]) store8<float>(dst + c * 256, &acc[r][c * 8]);
+      if (blockIdx.y == 0 && lane == 0) p.db_acc[v] = gsum[r];
+    }
   }
 }
 
 // ------------------------------------------------------------------ K3a: route
-// One CTA per batch row b.  Stable counting sort of the active pairs of row b
-// by key s = I[b,v]: the vocabulary is cut into `nseg` contiguous segments,
+// Grid (window, b).  The vocabulary is cut into windows of RT_WIN rows; for
+// each (b, window) the CTA performs a stable counting sort of the window's
+// active pairs by key s = I[b,v] entirely in shared memory and writes the
+// sorted (v, g) run out contiguously (coalesced), with per-(b, window, s)
+// offsets.  Stability: the window is split into `nseg` contiguous segments,
 // one per warp; per-(segment, s) counts give every warp its own cursors, and
-// within a warp equal keys are ranked by lane order (match.any), so each
-// (b, s) list ends up in ascending v.  Output: pairs[b*V + k] = (v, g bits),
-// offsets[b*(S+1) + s] = start of list s (offsets[..S] = number of pairs).
-__global__ void __launch_bounds__(ROUTE_THREADS)
-sparton_bwd_route_kernel(const BwdParams p, int nseg) {
-  extern __shared__ int hist[];            // [nseg][S] (+ scan scratch)
-  const int b = blockIdx.x;
+// equal keys inside a warp are ranked by lane order (match.any), so every
+// (b, window, s) sub-list is in ascending v.
+constexpr int RT_THREADS = 512;
+constexpr int RT_WIN = 8192;
+constexpr int RT_SMEM_BUDGET = 200 * 1024;
+
+__global__ void __launch_bounds__(RT_THREADS)
+sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin) {
+  extern __shared__ int4 rt_smem[];
+  const int S = p.S;
+  int2* ent = reinterpret_cast<int2*>(rt_smem);       // [RT_WIN] sorted (v, g)
+  int* hist = reinterpret_cast<int*>(ent + RT_WIN);   // [nseg][S]
+  int* scan_tmp = hist + nseg * S;                    // [32]
+  const int w = blockIdx.x;
+  const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int S = p.S;
-  int* scan_tmp = hist + nseg * S;         // [32] warp totals for the block scan
+  const int v0 = w * RT_WIN;
+  const int n = min(RT_WIN, p.V - v0);
+  const int seg_len = (n + nseg - 1) / nseg;
 
-  for (int i = threadIdx.x; i < nseg * S; i += ROUTE_THREADS) hist[i] = 0;
+  for (int i = threadIdx.x; i < nseg * S; i += RT_THREADS) hist[i] = 0;
   __syncthreads();
 
-  const float* Yb = p.Y + (size_t)b * p.ldY;
-  const int32_t* Ib = p.I + (size_t)b * p.ldY;
-  const long long seg_len = ((long long)p.V + nseg - 1) / nseg;
+  const float* Yb = p.Y + (size_t)b * p.ldY + v0;
+  const int32_t* Ib = p.I + (size_t)b * p.ldY + v0;
+  const float* dYb = p.dY + (size_t)b * p.ldDY + v0;
 
-  // Phase 1: per-segment histograms.
+  // Phase 1: per-segment histograms (4 x 32 loads in flight per warp).
   if (warp < nseg) {
-    const int vs = (int)min((long long)p.V, warp * seg_len);
-    const int ve = (int)min((long long)p.V, (warp + 1) * seg_len);
+    const int vs = min(n, warp * seg_len), ve = min(n, (warp + 1) * seg_len);
     int* h = hist + warp * S;
-    for (int v = vs + lane; v < ve; v += 32) {
-      if (Yb[v] > 0.f) atomicAdd(&h[Ib[v]], 1);
+    for (int base = vs; base < ve; base += 128) {
+      float y[4];
+      int k[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int v = base + q * 32 + lane;
+        y[q] = v < ve ? Yb[v] : 0.f;
+        k[q] = v < ve ? Ib[v] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (y[q] > 0.f) atomicAdd(&h[k[q]], 1);
     }
   }
   __syncthreads();
 
-  // Phase 2: exclusive scan over s of the per-s totals (block-wide), then
-  // per-s exclusive scan over segments -> cursors, written back into hist.
-  int* off = p.offsets + (size_t)b * (S + 1);
+  // Phase 2: exclusive scan over s of the per-s totals -> window-local list
+  // offsets; then per-s exclusive scan over segments -> cursors (in hist).
+  int* off = p.offsets + ((size_t)b * nwin + w) * (S + 1);
   int carry = 0;
-  for (int s0 = 0; s0 < S; s0 += ROUTE_THREADS) {
+  for (int s0 = 0; s0 < S; s0 += RT_THREADS) {
     const int s = s0 + threadIdx.x;
     int tot = 0;
     if (s < S)
-      for (int w = 0; w < nseg; ++w) tot += hist[w * S + s];
-    // inclusive warp scan
+      for (int q = 0; q < nseg; ++q) tot += hist[q * S + s];
     int x = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -211,69 +350,80 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg) {
     if (lane == 31) scan_tmp[warp] = x;
     __syncthreads();
     if (warp == 0) {
-      int t = scan_tmp[lane];
+      int t = lane < RT_THREADS / 32 ? scan_tmp[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, t, o);
         if (lane >= o) t += y;
       }
-      scan_tmp[lane] = t;   // inclusive warp-total prefix
+      if (lane < RT_THREADS / 32) scan_tmp[lane] = t;
     }
     __syncthreads();
     const int excl = carry + (warp > 0 ? scan_tmp[warp - 1] : 0) + x - tot;
     if (s < S) {
       off[s] = excl;
       int cur = excl;
-      for (int w = 0; w < nseg; ++w) {
-        const int c = hist[w * S + s];
-        hist[w * S + s] = cur;
+      for (int q = 0; q < nseg; ++q) {
+        const int c = hist[q * S + s];
+        hist[q * S + s] = cur;
         cur += c;
       }
     }
-    carry += scan_tmp[31];
+    carry += scan_tmp[RT_THREADS / 32 - 1];
     __syncthreads();
   }
   if (threadIdx.x == 0) off[S] = carry;
-  __syncthreads();
+  const int total = carry;
 
-  // Phase 3: stable scatter of (v, g) into the per-s lists.
+  // Phase 3: stable scatter of (v, g) into shared memory.
   if (warp < nseg) {
-    const int vs = (int)min((long long)p.V, warp * seg_len);
-    const int ve = (int)min((long long)p.V, (warp + 1) * seg_len);
+    const int vs = min(n, warp * seg_len), ve = min(n, (warp + 1) * seg_len);
     int* cur = hist + warp * S;
-    int2* out = p.pairs + (size_t)b * p.V;
-    const float* dYb = p.dY + (size_t)b * p.ldDY;
-    for (int base = vs; base < ve; base += 32) {
-      const int v = base + lane;
-      bool active = false;
-      int key = 0;
-      float g = 0.f;
-      if (v < ve) {
-        const float y = Yb[v];
-        if (y > 0.f) {
-          active = true;
-          key = Ib[v];
-          g = pair_grad(y, dYb[v]);
+    for (int base = vs; base < ve; base += 128) {
+      float y[4], dy[4];
+      int k[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int v = base + q * 32 + lane;
+        const bool in = v < ve;
+        y[q] = in ? Yb[v] : 0.f;
+        k[q] = in ? Ib[v] : 0;
+        dy[q] = in ? dYb[v] : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool active = y[q] > 0.f;
+        const unsigned amask = __ballot_sync(0xffffffffu, active);
+        if (active) {
+          const unsigned peers = __match_any_sync(amask, k[q]);
+          const int rank = __popc(peers & ((1u << lane) - 1u));
+          const int pos = cur[k[q]] + rank;
+          ent[pos] = make_int2(v0 + base + q * 32 + lane, __float_as_int(pair_grad(y[q], dy[q])));
+          __syncwarp(amask);
+          if (rank == 0) cur[k[q]] += __popc(peers);
         }
+        __syncwarp();
       }
-      const unsigned amask = __ballot_sync(0xffffffffu, active);
-      if (active) {
-        const unsigned peers = __match_any_sync(amask, key);
-        const int rank = __popc(peers & ((1u << lane) - 1u));
-        const int pos = cur[key] + rank;
-        out[pos] = make_int2(v, __float_as_int(g));
-        __syncwarp(amask);
-        if (rank == 0) cur[key] += __popc(peers);
-      }
-      __syncwarp();
     }
   }
+  __syncthreads();
+
+  // Phase 4: coalesced copy-out of the sorted window.
+  int2* out = p.pairs + (size_t)b * p.V + v0;
+  for (int i = threadIdx.x; i < total; i += RT_THREADS) out[i] = ent[i];
 }
 
 // ------------------------------------------------------------------ K3b: dH
+// Warp owns one (b, s) row (x D slice).  The vocabulary is processed in
+// L2-sized chunks of `wpc` route windows (~40 MB of E) by successive launches,
+// so the E rows every resident warp gathers come from the same window of E.
+// Within a chunk the warp walks its (b, window, s) sub-lists in window order,
+// each in ascending v, so the accumulation order is exactly the reference's
+// (v ascending, hidden_row / np.add.at).  Partial sums carry across launches in
+// fp32 (the output itself when it is fp32, else the workspace accumulator).
 template <int CPL, typename OutT>
 __global__ void __launch_bounds__(DH_THREADS)
-sparton_bwd_dh_kernel(const BwdParams p) {
+sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long rowid = (long long)blockIdx.x * (DH_THREADS / 32) + warp;   // b*S + s
@@ -281,85 +431,132 @@ sparton_bwd_dh_kernel(const BwdParams p) {
   const int b = (int)(rowid / p.S);
   const int s = (int)(rowid - (long long)b * p.S);
   const int d0 = blockIdx.y * (256 * CPL);
-  const int* off = p.offsets + (size_t)b * (p.S + 1);
-  const int k0 = off[s], k1 = off[s + 1];
-  const int2* lst = p.pairs + (size_t)b * p.V;
+  const bool first = chunk == 0;
+  const bool last = chunk == p.nchunks - 1;
+  const int w0 = chunk * p.wpc;
+  const int w1 = min(p.nwin, w0 + p.wpc);
 
   bool dvalid[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) dvalid[c] = (d0 + c * 256 + lane * 8) < p.D;
   float acc[CPL * 8];
+  float* accg = p.acc32 ? p.acc32 : reinterpret_cast<float*>(p.dH);   // fp32 carry buffer
+  if (first) {
 #pragma unroll
-  for (int i = 0; i < CPL * 8; ++i) acc[i] = 0.f;
-
-  for (int kb = k0; kb < k1; kb += 32) {
-    const int n = min(32, k1 - kb);
-    int2 mine = make_int2(0, 0);
-    if (lane < n) mine = lst[kb + lane];
-    int j = 0;
-    for (; j + 2 <= n; j += 2) {
-      const int va = __shfl_sync(0xffffffffu, mine.x, j);
-      const float ga = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j));
-      const int vb = __shfl_sync(0xffffffffu, mine.x, j + 1);
-      const float gb = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j + 1));
-      const __nv_bfloat16* ra = p.E + (size_t)va * p.D + d0 + lane * 8;
-      const __nv_bfloat16* rb = p.E + (size_t)vb * p.D + d0 + lane * 8;
-      int4 xa[CPL], xb[CPL];
+    for (int i = 0; i < CPL * 8; ++i) acc[i] = 0.f;
+  } else {
+    const float* src = accg + (size_t)rowid * p.D + d0 + lane * 8;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        xa[c] = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(ra + c * 256)) : make_int4(0, 0, 0, 0);
-        xb[c] = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(rb + c * 256)) : make_int4(0, 0, 0, 0);
-      }
-      // ascending v: a before b
+    for (int c = 0; c < CPL; ++c) {
+      if (dvalid[c]) {
+        const float4 a = *reinterpret_cast<const float4*>(src + c * 256);
+        const float4 bq = *reinterpret_cast<const float4*>(src + c * 256 + 4);
+        acc[c * 8 + 0] = a.x; acc[c * 8 + 1] = a.y; acc[c * 8 + 2] = a.z; acc[c * 8 + 3] = a.w;
+        acc[c * 8 + 4] = bq.x; acc[c * 8 + 5] = bq.y; acc[c * 8 + 6] = bq.z; acc[c * 8 + 7] = bq.w;
+      } else {
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) fma8(&acc[c * 8], ga, xa[c]);
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) fma8(&acc[c * 8], gb, xb[c]);
-    }
-    if (j < n) {
-      const int va = __shfl_sync(0xffffffffu, mine.x, j);
-      const float ga = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j));
-      const __nv_bfloat16* ra = p.E + (size_t)va * p.D + d0 + lane * 8;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int4 xa = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(ra + c * 256)) : make_int4(0, 0, 0, 0);
-        fma8(&acc[c * 8], ga, xa);
+        for (int i = 0; i < 8; ++i) acc[c * 8 + i] = 0.f;
       }
     }
   }
-  OutT* dst = reinterpret_cast<OutT*>(p.dH) + (size_t)rowid * p.D + d0 + lane * 8;
+
+  for (int w = w0; w < w1; ++w) {
+    const int* off = p.offsets + ((size_t)b * p.nwin + w) * (p.S + 1);
+    const int k1 = off[s + 1];
+    const int2* lst = p.pairs + (size_t)b * p.V + (size_t)w * RT_WIN;
+    for (int k = off[s]; k < k1; k += 32) {
+      const int m = min(32, k1 - k);
+      int2 mine = make_int2(0, 0);
+      if (lane < m) mine = lst[k + lane];
+      int j = 0;
+      for (; j + DH_UNROLL <= m; j += DH_UNROLL) {
+        float gq[DH_UNROLL];
+        int4 xq[DH_UNROLL][CPL];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c)
-    if (dvalid[c]) store8<OutT>(dst + c * 256, &acc[c * 8]);
+        for (int q = 0; q < DH_UNROLL; ++q) {
+          const int vq = __shfl_sync(0xffffffffu, mine.x, j + q);
+          gq[q] = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j + q));
+          const __nv_bfloat16* r = p.E + (size_t)vq * p.D + d0 + lane * 8;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            xq[q][c] = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < DH_UNROLL; ++q) {
+          const uint64_t gg = pack_gg(gq[q]);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) fma8(&acc[c * 8], gg, xq[q][c]);
+        }
+      }
+      for (; j < m; ++j) {
+        const int va = __shfl_sync(0xffffffffu, mine.x, j);
+        const float ga = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j));
+        const __nv_bfloat16* r = p.E + (size_t)va * p.D + d0 + lane * 8;
+        const uint64_t gg = pack_gg(ga);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int4 x = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
+          fma8(&acc[c * 8], gg, x);
+        }
+      }
+    }
+  }
+
+  if (last) {
+    OutT* dst = reinterpret_cast<OutT*>(p.dH) + (size_t)rowid * p.D + d0 + lane * 8;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (dvalid[c]) store8<OutT>(dst + c * 256, &acc[c * 8]);
+  } else {
+    float* dst = accg + (size_t)rowid * p.D + d0 + lane * 8;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (dvalid[c]) store8<float>(dst + c * 256, &acc[c * 8]);
+  }
 }
+
+int route_nseg(int S) {
+  int nseg = (RT_SMEM_BUDGET - RT_WIN * 8 - 128) / (S * 4);
+  if (nseg > RT_THREADS / 32) nseg = RT_THREADS / 32;
+  if (nseg < 1) nseg = 1;
+  return nseg;
+}
+size_t route_smem_bytes(int S, int nseg) { return (size_t)RT_WIN * 8 + ((size_t)nseg * S + 32) * 4; }
 
 template <int CPL, typename OutT>
 int launch_bwd_t(const BwdParams& p, cudaStream_t stream) {
   const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
   {
+    constexpr int smem = DeCfg<CPL>::SMEM_BYTES;
+    cudaError_t e = cudaFuncSetAttribute(sparton_bwd_de_kernel<CPL, OutT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de)", e);
     dim3 grid((p.V + DE_VB - 1) / DE_VB, dslices);
-    sparton_bwd_de_kernel<CPL, OutT><<<grid, DE_THREADS, 0, stream>>>(p);
-    cudaError_t e = cudaGetLastError();
+    for (int b0 = 0; b0 < p.B; b0 += p.bchunk) {
+      sparton_bwd_de_kernel<CPL, OutT><<<grid, DE_THREADS, smem, stream>>>(p, b0, min(p.B, b0 + p.bchunk));
+      e = cudaGetLastError();
+      if (e != cudaSuccess) break;
+    }
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_de_kernel", e);
   }
   {
-    int nseg = ROUTE_SMEM_INTS / (p.S > 0 ? p.S : 1);
-    if (nseg > 32) nseg = 32;
-    if (nseg < 1) nseg = 1;
-    const size_t smem = ((size_t)nseg * p.S + 32) * sizeof(int);
+    const int nseg = route_nseg(p.S);
+    const size_t smem = route_smem_bytes(p.S, nseg);
     cudaError_t e = cudaFuncSetAttribute(sparton_bwd_route_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(route)", e);
-    sparton_bwd_route_kernel<<<p.B, ROUTE_THREADS, smem, stream>>>(p, nseg);
+    sparton_bwd_route_kernel<<<dim3(p.nwin, p.B), RT_THREADS, smem, stream>>>(p, nseg, p.nwin);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_route_kernel", e);
   }
   {
     const long long rows = (long long)p.B * p.S;
     dim3 grid((unsigned)((rows + DH_THREADS / 32 - 1) / (DH_THREADS / 32)), dslices);
-    sparton_bwd_dh_kernel<CPL, OutT><<<grid, DH_THREADS, 0, stream>>>(p);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
+    for (int c = 0; c < p.nchunks; ++c) {
+      sparton_bwd_dh_kernel<CPL, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
+    }
   }
   return SPARTON_OK;
 }
@@ -367,19 +564,47 @@ int launch_bwd_t(const BwdParams& p, cudaStream_t stream) {
 template <typename OutT>
 int launch_bwd_dtype(const BwdParams& p, cudaStream_t stream) {
   if (p.D <= 256) return launch_bwd_t<1, OutT>(p, stream);
-  if (p.D <= 512) return launch_bwd_t<2, OutT>(p, stream);
-  if (p.D <= 768) return launch_bwd_t<3, OutT>(p, stream);
-  return launch_bwd_t<4, OutT>(p, stream);
+  if (p.D <= 512 || p.D > 768) return launch_bwd_t<2, OutT>(p, stream);
+  return launch_bwd_t<3, OutT>(p, stream);
 }
 
 }  // namespace
 
-int bwd_max_seq() { return ROUTE_SMEM_INTS - 32; }
+// Largest S the in-smem route supports (one segment of S counters + the window).
+int bwd_max_seq() { return (RT_SMEM_BUDGET - RT_WIN * 8 - 128) / 4; }
 
-size_t bwd_workspace_bytes(long long B, long long S, long long V) {
-  const size_t pairs = (size_t)B * (size_t)V * sizeof(int2);
-  const size_t offs = (size_t)B * (size_t)(S + 1) * sizeof(int);
-  return ((pairs + 255) & ~size_t(255)) + ((offs + 255) & ~size_t(255));
+// E chunk per dH pass: ~40 MB of bf16 rows so it stays L2-resident (126 MB L2)
+// next to the streaming pair lists and accumulators.
+constexpr long long DH_CHUNK_BYTES = 40ll << 20;
+constexpr long long DE_CHUNK_BYTES = 48ll << 20;
+
+BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long long V, int grad_dtype) {
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  BwdWorkspace w{};
+  w.nwin = (int)((V + RT_WIN - 1) / RT_WIN);
+  long long wpc = DH_CHUNK_BYTES / ((long long)RT_WIN * D * 2);
+  if (wpc < 1) wpc = 1;
+  if (wpc > w.nwin) wpc = w.nwin;
+  w.wpc = (int)wpc;
+  w.nchunks = (w.nwin + w.wpc - 1) / w.wpc;
+  w.pairs = 0;
+  w.offsets = up((size_t)B * (size_t)V * sizeof(int2));
+  // dE passes over batch chunks of ~48 MB of H (L2-resident while every
+  // vocab block of the pass gathers from it).
+  long long bc = DE_CHUNK_BYTES / (S * D * 2 > 0 ? S * D * 2 : 1);
+  if (bc < DE_BC) bc = DE_BC;
+  if (bc > B) bc = B;
+  w.bchunk = (int)bc;
+  const int de_passes = (int)((B + bc - 1) / bc);
+  w.db_acc = w.offsets + up((size_t)B * (size_t)w.nwin * (size_t)(S + 1) * sizeof(int));
+  w.dE_acc = w.db_acc + up((size_t)V * sizeof(float));
+  const bool need_de_acc = grad_dtype == SPARTON_BF16 && de_passes > 1;
+  w.acc32 = w.dE_acc + (need_de_acc ? up((size_t)V * (size_t)D * sizeof(float)) : 0);
+  const bool need_acc = grad_dtype == SPARTON_BF16 && w.nchunks > 1;
+  w.total = w.acc32 + (need_acc ? up((size_t)B * (size_t)S * (size_t)D * sizeof(float)) : 0);
+  if (!need_acc) w.acc32 = (size_t)-1;
+  if (!need_de_acc) w.dE_acc = (size_t)-1;
+  return w;
 }
 
 int launch_bwd(const BwdParams& p, int grad_dtype, cudaStream_t stream) {

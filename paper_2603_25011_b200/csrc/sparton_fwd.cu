@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cmath>
+#include <cstdlib>
 
 #include "ptx.cuh"
 #include "sparton_internal.h"
@@ -51,15 +52,53 @@ struct FwdCfg {
   static constexpr int SMEM_BYTES = NST * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
-__device__ __forceinline__ void unit_coords(long long u, const FwdParams& p, int& b, int& vt) {
-  const long long per_group = (long long)p.group_vt * p.B;
-  const long long g = u / per_group;
-  const long long r = u - g * per_group;
-  const int gv0 = (int)g * p.group_vt;
-  const int gsz = min(p.group_vt, p.num_vt - gv0);
-  b = (int)(r / gsz);
-  vt = gv0 + (int)(r % gsz);
-}
+// Per-cluster unit sequence (all warp roles walk the same one).
+//
+// Large B (B >= 2 * clusters): vocab tiles are grouped (~48 MB of E per
+// group); inside a group, cluster c owns the batch rows b = c' + j*nclusters
+// (c' = a per-group rotation of c) and, for each of them, walks every vocab
+// tile of the group.  H[b] is therefore pulled into L2 once and reused for the
+// whole group by one cluster, while the group's E tiles are shared by all
+// clusters; clusters never need to stay in lock-step (no drift-induced
+// thrashing), and H streams from HBM once per group.
+// Default / small B: round-robin over units ordered (vocab group, b, tile).
+struct UnitIter {
+  int g = 0, j = 0, k = 0;
+  long long u = 0;
+  int c, nc;
+  __device__ UnitIter(int cluster, int nclusters) : c(cluster), nc(nclusters) { u = cluster; }
+  __device__ __forceinline__ bool next(const FwdParams& p, int& b, int& vt) {
+    if (!p.sched_bgroups) {
+      // Round-robin over units ordered (vocab group, b, tile): consecutive
+      // clusters share H[b] and the group's E tiles stay L2-resident.
+      if (u >= p.num_units) return false;
+      const long long per_group = (long long)p.group_vt * p.B;
+      const long long gg = u / per_group;
+      const long long r = u - gg * per_group;
+      const int gv0 = (int)gg * p.group_vt;
+      const int gsz = min(p.group_vt, p.num_vt - gv0);
+      b = (int)(r / gsz);
+      vt = gv0 + (int)(r % gsz);
+      u += nc;
+      return true;
+    }
+    while (true) {
+      const int g0 = g * p.group_vt;
+      if (g0 >= p.num_vt) return false;
+      const int gsz = min(p.group_vt, p.num_vt - g0);
+      const int bb = j * nc + (int)(((long long)c + (long long)g * p.rot) % nc);
+      if (bb < p.B) {
+        b = bb;
+        vt = g0 + k;
+        if (++k == gsz) { k = 0; ++j; }
+        return true;
+      }
+      ++g;
+      j = 0;
+      k = 0;
+    }
+  }
+};
 
 // Reduce 32 accumulator columns (tile columns c0..c0+31 of the current chunk)
 // into four interleaved running (max, argmax) pairs; column c goes to slot c&3.
@@ -132,13 +171,13 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
-      const uint64_t pol_e = ptx::policy_evict_last();
+      const uint64_t pol_e = p.e_evict_last ? ptx::policy_evict_last() : ptx::policy_evict_normal();
       const uint64_t pol_h = ptx::policy_evict_normal();
       int st = 0;
       uint32_t ph = 0;
-      for (long long u = cluster; u < p.num_units; u += nclusters) {
-        int b, vt;
-        unit_coords(u, p, b, vt);
+      UnitIter it((int)cluster, (int)nclusters);
+      int b, vt;
+      while (it.next(p, b, vt)) {
         const int vrow = vt * C::TILE_V + (int)rank * C::BM;
         for (int sc = 0; sc < nsc; ++sc) {
           const int hrow = b * p.S + sc * C::SN + (int)rank * C::BN_CTA;
@@ -169,7 +208,9 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (long long u = cluster; u < p.num_units; u += nclusters) {
+      UnitIter it((int)cluster, (int)nclusters);
+      int b, vt;
+      while (it.next(p, b, vt)) {
         for (int sc = 0; sc < nsc; ++sc) {
           ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), aph ^ 1);
           ptx::tc_fence_after();
@@ -199,17 +240,17 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
     const int row = q * 32 + (int)lane;           // vocab row within this CTA's tile
     const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
-    uint32_t tempty_addr[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint32_t a = ptx::smem_u32(&tempty[i]);
-      tempty_addr[i] = (CG == 2) ? ptx::mapa(a, 0) : a;
+    uint32_t tempty0 = ptx::smem_u32(&tempty[0]);
+    uint32_t tempty1 = ptx::smem_u32(&tempty[1]);
+    if constexpr (CG == 2) {
+      tempty0 = ptx::mapa(tempty0, 0);
+      tempty1 = ptx::mapa(tempty1, 0);
     }
     int acc = 0;
     uint32_t aph = 0;
-    for (long long u = cluster; u < p.num_units; u += nclusters) {
-      int b, vt;
-      unit_coords(u, p, b, vt);
+    UnitIter it((int)cluster, (int)nclusters);
+    int b, vt;
+    while (it.next(p, b, vt)) {
       const int v = vt * C::TILE_V + (int)rank * C::BM + row;
       const float bv = (v < p.V) ? __ldg(p.bias + v) : 0.0f;
       const uint8_t* mrow = p.mask + (size_t)b * p.S;
@@ -244,8 +285,9 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (CG == 2) ptx::mbar_arrive_cluster(tempty_addr[acc]);
-          else ptx::mbar_arrive(tempty_addr[acc]);
+          const uint32_t te = acc ? tempty1 : tempty0;
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster(te);
+          else ptx::mbar_arrive(te);
         }
         acc ^= 1;
         if (acc == 0) aph ^= 1;
@@ -311,19 +353,28 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
   return SPARTON_OK;
 }
 
+static int gcd_int(int a, int b) { while (b) { const int t = a % b; a = b; b = t; } return a; }
+
 int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cta_group,
                int num_sms, cudaStream_t stream) {
   const int tile_v = 128 * cta_group;
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
-  // L2 rasterisation: walk a group of vocab tiles (~24 MB of E) for every batch
-  // row before moving on, so the group of E stays L2-resident while H[b] is
-  // shared by all CTAs working on the same b.
-  long long tile_bytes = (long long)tile_v * prm.D * 2;
-  int gv = (int)((24ll << 20) / (tile_bytes > 0 ? tile_bytes : 1));
+  prm.num_units = (long long)prm.num_vt * prm.B;
+  const int nclusters = max(1, num_sms / cta_group);
+  // E group of ~48 MB stays L2-resident while H streams (see UnitIter).
+  const long long tile_bytes = (long long)tile_v * prm.D * 2;
+  long long group_bytes = 24ll << 20;
+  if (const char* ev = getenv("SPARTON_FWD_GROUP_KB")) group_bytes = atoll(ev) << 10;
+  int gv = (int)(group_bytes / (tile_bytes > 0 ? tile_bytes : 1));
   if (gv < 1) gv = 1;
   if (gv > prm.num_vt) gv = prm.num_vt;
   prm.group_vt = gv;
-  prm.num_units = (long long)prm.num_vt * prm.B;
+  prm.sched_bgroups = 0;   // measured: the grouped round-robin moves less DRAM (profiles/)
+  if (const char* ev = getenv("SPARTON_FWD_SCHED")) prm.sched_bgroups = ev[0] == '1';
+  int rot = (int)(0.618 * nclusters + 0.5);
+  if (rot < 1) rot = 1;
+  while (gcd_int(rot, nclusters) != 1) ++rot;
+  prm.rot = rot % nclusters;
   if (cta_group == 2) return launch_fwd_impl<2>(tmE, tmH, prm, num_sms, stream);
   return launch_fwd_impl<1>(tmE, tmH, prm, num_sms, stream);
 }

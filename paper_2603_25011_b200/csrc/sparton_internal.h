@@ -21,6 +21,9 @@ struct FwdParams {
   int num_vt;          // number of vocab tiles
   int group_vt;        // vocab tiles per L2 rasterisation group
   long long num_units; // num_vt * B
+  int e_evict_last;    // L2 policy for E tiles (experiment switch)
+  int sched_bgroups;   // 1: batch-row-per-cluster groups (large B), 0: round-robin units
+  int rot;             // per-group rotation of the cluster -> batch-row assignment
 };
 
 struct BwdParams {
@@ -36,8 +39,23 @@ struct BwdParams {
   long long ldY, ldDY;
   int include_bias_grad;
   int2* pairs;         // workspace: per-b argmax-routed (v, g) lists, B*V entries
-  int* offsets;        // workspace: B*(S+1) list offsets
+  int* offsets;        // workspace: B*nwin*(S+1) per-(b, window, s) list offsets
+  float* acc32;        // workspace: fp32 dH accumulator (bf16 output, >1 chunk) or nullptr
+  float* dE_acc;       // workspace: fp32 dE carry across batch-chunk passes (bf16 output) or nullptr
+  float* db_acc;       // workspace: fp32 db carry across batch-chunk passes
+  int bchunk;          // batch rows per dE pass (H chunk kept L2-resident)
+  int de_stagger;      // experiment switch: rotate each CTA's batch order
+  int nwin;            // route windows (RT_WIN vocab rows each)
+  int wpc;             // route windows per dH pass (E chunk kept L2-resident)
+  int nchunks;         // dH passes
 };
+
+// Workspace layout for sparton_bwd (byte offsets, 256-B aligned).
+struct BwdWorkspace {
+  size_t pairs, offsets, db_acc, dE_acc, acc32, total;
+  int nwin, wpc, nchunks, bchunk;
+};
+BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long long V, int grad_dtype);
 
 // Records a thread-local error message and returns the status code.
 int set_error(int code, const char* msg);
@@ -47,7 +65,6 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
                int num_sms, cudaStream_t stream);
 int fwd_smem_bytes(int cta_group);
 int launch_bwd(const BwdParams& prm, int grad_dtype, cudaStream_t stream);
-size_t bwd_workspace_bytes(long long B, long long S, long long V);
 int bwd_max_seq();
 
 }  // namespace sparton

@@ -103,8 +103,9 @@ def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: 
     return Y, I
 
 
-def bwd_workspace_bytes(B: int, S: int, V: int) -> int:
-    return int(_lib.load().sparton_bwd_workspace_bytes(B, S, V))
+def bwd_workspace_bytes(B: int, S: int, D: int, V: int, grad_dtype: torch.dtype = torch.float32) -> int:
+    gd = _lib.SPARTON_BF16 if grad_dtype == torch.bfloat16 else _lib.SPARTON_F32
+    return int(_lib.load().sparton_bwd_workspace_bytes(B, S, D + (-D) % 8, V, gd))
 
 
 @torch.no_grad()
@@ -143,9 +144,9 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     dE = torch.empty((V, Dp), dtype=grad_dtype, device=dev)
     db = torch.empty((V,), dtype=torch.float32, device=dev)
     lib = _lib.load()
-    ws_bytes = int(lib.sparton_bwd_workspace_bytes(B, S, V))
-    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
     gd = _lib.SPARTON_BF16 if grad_dtype == torch.bfloat16 else _lib.SPARTON_F32
+    ws_bytes = int(lib.sparton_bwd_workspace_bytes(B, S, Dp, V, gd))
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
     with torch.cuda.device(dev):
         rc = lib.sparton_bwd(Hp.data_ptr(), Ep.data_ptr(), Y.data_ptr(), I.data_ptr(), dY.data_ptr(),
                              dH.data_ptr(), dE.data_ptr(), db.data_ptr(), B, S, Dp, V, Y.stride(0),

@@ -37,11 +37,19 @@ def test_library_exports_every_declared_symbol():
 def test_workspace_formula():
     from paper_2603_25011_b200 import _lib
     lib = _lib.load()
-    B, S, V = 512, 512, 250002
-    pairs = (B * V * 8 + 255) // 256 * 256
-    offs = (B * (S + 1) * 4 + 255) // 256 * 256
-    assert lib.sparton_bwd_workspace_bytes(B, S, V) == pairs + offs
-    assert lib.sparton_bwd_workspace_bytes(0, S, V) == 0
+    up = lambda x: (x + 255) // 256 * 256
+    win = 8192                                   # route window (vocab rows)
+    B, S, D, V = 512, 512, 768, 250002
+    nwin = -(-V // win)
+    base = up(B * V * 8) + up(B * nwin * (S + 1) * 4) + up(V * 4)
+    # fp32 gradients carry partial sums in the outputs; bf16 needs fp32 carries
+    # because dE runs in batch-chunk passes (H chunk L2-resident) and dH in
+    # vocab-chunk passes (cfg3: 384 MB of E).
+    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_F32) == base
+    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_BF16) == base + up(V * D * 4) + up(B * S * D * 4)
+    # a tiny problem is one window and one pass of each kind: no carry buffers
+    assert lib.sparton_bwd_workspace_bytes(2, 3, 8, 5, _lib.SPARTON_BF16) == up(2 * 5 * 8) + up(2 * 1 * 4 * 4) + up(5 * 4)
+    assert lib.sparton_bwd_workspace_bytes(0, S, D, V, 0) == 0
 
 
 @pytest.mark.parametrize("dims", [(0, 3, 8, 5), (2, 3, 4, 5), (2, -1, 8, 5)])
