@@ -112,7 +112,7 @@ struct DeCfg {
   static constexpr int NST = CPL >= 3 ? 4 : (CPL == 2 ? 6 : 8);
   static constexpr int WARP_STAGE_BYTES = DE_RPW * ROW_BYTES;  // DE_RPW rows per warp per stage
   static constexpr int RING_BYTES = DE_WARPS * NST * WARP_STAGE_BYTES;
-  static constexpr int GI_BYTES = 2 * 2 * DE_BC * DE_VB * 4;  // g and I, double buffered
+  static constexpr int GI_BYTES = 2 * DE_BC * DE_VB * 8;      // (I, g) pairs, double buffered
   static constexpr int BAR_BYTES = DE_WARPS * NST * 8;
   static constexpr int SMEM_BYTES = RING_BYTES + GI_BYTES + BAR_BYTES;
 };
@@ -122,7 +122,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
-template <int CPL, typename OutT>
+template <int CPL, bool FULL, typename OutT>
 __global__ void __launch_bounds__(DE_THREADS, 1)
 sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   using C = DeCfg<CPL>;
@@ -130,32 +130,33 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint8_t* ring = de_smem + (size_t)warp * C::NST * C::WARP_STAGE_BYTES;       // this warp's ring
-  float* g_s = reinterpret_cast<float*>(de_smem + C::RING_BYTES);               // [2][BC][VB]
-  int* i_s = reinterpret_cast<int*>(g_s + 2 * DE_BC * DE_VB);                   // [2][BC][VB]
+  int2* gi_s = reinterpret_cast<int2*>(de_smem + C::RING_BYTES);                // [2][BC][VB] (idx, g)
   uint64_t* bars = reinterpret_cast<uint64_t*>(de_smem + C::RING_BYTES + C::GI_BYTES) + warp * C::NST;
 
   const int v0 = blockIdx.x * DE_VB;
   const int d0 = blockIdx.y * C::DS;
-  const uint32_t slice_bytes = (uint32_t)min(C::DS, p.D - d0) * 2u;
+  const uint32_t slice_bytes = FULL ? (uint32_t)C::ROW_BYTES : (uint32_t)min(C::DS, p.D - d0) * 2u;
   const int nb = bend - bbeg;                // batch rows of this pass (local index lb = b - bbeg)
-  const int rot = p.de_stagger ? (int)(blockIdx.x % (unsigned)nb) : 0;   // experiment: rotated start
   const bool first = bbeg == 0;
   const bool last = bend == p.B;
 
+  // Rows of inactive pairs are never copied: the ring must hold finite values
+  // so that g = 0 times the stale row adds exactly nothing.
+  for (int i = lane; i < C::NST * C::WARP_STAGE_BYTES / 16; i += 32)
+    reinterpret_cast<int4*>(ring)[i] = make_int4(0, 0, 0, 0);
   if (lane == 0) {
     for (int i = 0; i < C::NST; ++i) ptx::mbar_init(ptx::smem_u32(&bars[i]), 1);
     ptx::fence_mbar_init();
   }
 
-  // Stage g and I of local batch rows [lb0, lb0 + DE_BC) into buffer `buf`.
+  // Stage (I, g) of local batch rows [lb0, lb0 + DE_BC) into buffer `buf`.
   auto stage_gi = [&](int lb0, int buf) {
     for (int e = threadIdx.x; e < DE_BC * DE_VB; e += DE_THREADS) {
       const int bb = e / DE_VB, vv = e % DE_VB;
-      const int lq = lb0 + bb, v = v0 + vv;
+      const int lb = lb0 + bb, v = v0 + vv;
       float g = 0.f;
       int idx = -1;
-      if (lq < nb && v < p.V) {
-        const int lb = lq + rot < nb ? lq + rot : lq + rot - nb;
+      if (lb < nb && v < p.V) {
         const size_t b = (size_t)(bbeg + lb);
         const float y = p.Y[b * p.ldY + v];
         if (y > 0.f) {
@@ -163,22 +164,23 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
           idx = p.I[b * p.ldY + v];
         }
       }
-      g_s[(buf * DE_BC + bb) * DE_VB + vv] = g;
-      i_s[(buf * DE_BC + bb) * DE_VB + vv] = idx;
+      gi_s[(buf * DE_BC + bb) * DE_VB + vv] = make_int2(idx, __float_as_int(g));
     }
   };
-  // Lanes 0..DE_RPW-1 gather this warp's rows for local batch row lb into ring stage
-  // lb % NST (one bulk copy each); lane 0 arms the stage barrier with the total.
+  // Lanes 0..DE_RPW-1 gather this warp's rows for local batch row lb into ring
+  // stage lb % NST (one bulk copy each); lane 0 arms the stage barrier.
   auto issue = [&](int lb) {
     const int t = lb / DE_BC, bb = lb - t * DE_BC, buf = t & 1;
     const int st = lb % C::NST;
     const uint32_t bar = ptx::smem_u32(&bars[st]);
-    const int idx = lane < DE_RPW ? i_s[(buf * DE_BC + bb) * DE_VB + warp + DE_WARPS * lane] : -1;
+    const int idx = lane < DE_RPW ? gi_s[(buf * DE_BC + bb) * DE_VB + warp + DE_WARPS * lane].x : -1;
     const unsigned act = __ballot_sync(0xffffffffu, idx >= 0);
-    if (lane == 0) ptx::mbar_arrive_expect_tx(bar, (uint32_t)__popc(act) * slice_bytes);
+    if (lane == 0) {
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(bar, (uint32_t)__popc(act) * slice_bytes);
+    }
     if (idx >= 0) {
-      const int lbr = lb + rot < nb ? lb + rot : lb + rot - nb;
-      const size_t hrow = (size_t)(bbeg + lbr) * p.S + idx;
+      const size_t hrow = (size_t)(bbeg + lb) * p.S + idx;
       bulk_g2s(ptx::smem_u32(ring + st * C::WARP_STAGE_BYTES + lane * C::ROW_BYTES),
                p.H + hrow * (size_t)p.D + d0, slice_bytes, bar);
     }
@@ -188,7 +190,7 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   float gsum[DE_RPW];
   bool dvalid[CPL];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) dvalid[c] = (c * 256 + lane * 8) * 2 < (int)slice_bytes;
+  for (int c = 0; c < CPL; ++c) dvalid[c] = FULL || (c * 256 + lane * 8) * 2 < (int)slice_bytes;
   // fp32 carry from the previous pass (the fp32 output itself, or the workspace).
   float* carry = p.dE_acc ? p.dE_acc : reinterpret_cast<float*>(p.dE);
 #pragma unroll
@@ -216,7 +218,7 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   __syncthreads();
   // Prologue: NST-1 batch rows in flight (all within tiles 0/1, NST-1 < DE_BC).
   for (int lb = 0; lb < C::NST - 1 && lb < nb; ++lb) issue(lb);
-  uint32_t phase_bits = 0;   // parity per stage
+  const uint8_t* lane_src = ring + lane * 16;
 
   for (int lb = 0; lb < nb; ++lb) {
     const int t = lb / DE_BC, bb = lb - t * DE_BC, buf = t & 1;
@@ -228,28 +230,22 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
       __syncthreads();
     }
     // Issue local batch row lb+NST-1: its tile is t or t+1 (NST-1 < DE_BC), both resident.
-    if (lb + C::NST - 1 < nb) {
-      ptx::fence_proxy_async();
-      issue(lb + C::NST - 1);
-    }
+    if (lb + C::NST - 1 < nb) issue(lb + C::NST - 1);
     const int st = lb % C::NST;
-    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (phase_bits >> st) & 1u);
-    phase_bits ^= 1u << st;
-    const uint8_t* src = ring + st * C::WARP_STAGE_BYTES;
+    float g[DE_RPW];
+#pragma unroll
+    for (int r = 0; r < DE_RPW; ++r) g[r] = __int_as_float(gi_s[(buf * DE_BC + bb) * DE_VB + warp + DE_WARPS * r].y);
+    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (lb / C::NST) & 1);
+    const uint8_t* src = lane_src + st * C::WARP_STAGE_BYTES;
 #pragma unroll
     for (int r = 0; r < DE_RPW; ++r) {
-      const int vv = warp + DE_WARPS * r;
-      const int idx = i_s[(buf * DE_BC + bb) * DE_VB + vv];
-      if (idx >= 0) {
-        const float g = g_s[(buf * DE_BC + bb) * DE_VB + vv];
-        gsum[r] += g;
-        const uint64_t gg = pack_gg(g);
+      gsum[r] += g[r];
+      const uint64_t gg = pack_gg(g[r]);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          if (dvalid[c]) {
-            const int4 x = *reinterpret_cast<const int4*>(src + r * C::ROW_BYTES + (c * 256 + lane * 8) * 2);
-            fma8(&acc[r][c * 8], gg, x);
-          }
+      for (int c = 0; c < CPL; ++c) {
+        if (dvalid[c]) {
+          const int4 x = *reinterpret_cast<const int4*>(src + r * C::ROW_BYTES + c * 512);
+          fma8(&acc[r][c * 8], gg, x);
         }
       }
     }
@@ -523,21 +519,28 @@ int route_nseg(int S) {
 }
 size_t route_smem_bytes(int S, int nseg) { return (size_t)RT_WIN * 8 + ((size_t)nseg * S + 32) * 4; }
 
+template <int CPL, bool FULL, typename OutT>
+int launch_de(const BwdParams& p, cudaStream_t stream) {
+  constexpr int smem = DeCfg<CPL>::SMEM_BYTES;
+  cudaError_t e = cudaFuncSetAttribute(sparton_bwd_de_kernel<CPL, FULL, OutT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de)", e);
+  dim3 grid((p.V + DE_VB - 1) / DE_VB, (p.D + 256 * CPL - 1) / (256 * CPL));
+  for (int b0 = 0; b0 < p.B; b0 += p.bchunk) {
+    sparton_bwd_de_kernel<CPL, FULL, OutT><<<grid, DE_THREADS, smem, stream>>>(p, b0, min(p.B, b0 + p.bchunk));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_de_kernel", e);
+  }
+  return SPARTON_OK;
+}
+
 template <int CPL, typename OutT>
 int launch_bwd_t(const BwdParams& p, cudaStream_t stream) {
   const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
   {
-    constexpr int smem = DeCfg<CPL>::SMEM_BYTES;
-    cudaError_t e = cudaFuncSetAttribute(sparton_bwd_de_kernel<CPL, OutT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de)", e);
-    dim3 grid((p.V + DE_VB - 1) / DE_VB, dslices);
-    for (int b0 = 0; b0 < p.B; b0 += p.bchunk) {
-      sparton_bwd_de_kernel<CPL, OutT><<<grid, DE_THREADS, smem, stream>>>(p, b0, min(p.B, b0 + p.bchunk));
-      e = cudaGetLastError();
-      if (e != cudaSuccess) break;
-    }
-    if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_de_kernel", e);
+    const int rc = (p.D % (256 * CPL) == 0) ? launch_de<CPL, true, OutT>(p, stream)
+                                             : launch_de<CPL, false, OutT>(p, stream);
+    if (rc != SPARTON_OK) return rc;
   }
   {
     const int nseg = route_nseg(p.S);
