@@ -79,6 +79,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
                :: "r"(cluster_bar) : "memory");
 }
 
+// Relaxed variant: orders nothing but the arrival itself.  Used where the
+// hand-off only protects TMEM reads already retired by tcgen05.wait::ld (+
+// tcgen05.fence::before_thread_sync), so the release's MEMBAR.GPU — which
+// would wait for the thread's outstanding global stores — is unnecessary.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
+               :: "r"(cluster_bar) : "memory");
+}
+
 // Blocking wait on phase parity (try_wait suspends in hardware until the phase
 // flips or a system time limit passes).  Bounded: after 2^26 polls (seconds)
 // the kernel traps instead of hanging the device, so a protocol bug surfaces
@@ -130,6 +139,11 @@ __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t d
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_normal() {

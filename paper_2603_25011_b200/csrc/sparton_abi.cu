@@ -178,7 +178,7 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
   prm.ldY = ldY;
   {
     const char* ev = getenv("SPARTON_E_EVICT_LAST");
-    prm.e_evict_last = (ev && ev[0] == '0') ? 0 : 1;
+    prm.e_evict_last = ev ? atoi(ev) : 1;   // bits 0-1: E policy, bits 2-3: H policy
   }
   return launch_fwd(tmE, tmH, prm, cg, d.sms, static_cast<cudaStream_t>(stream));
 }

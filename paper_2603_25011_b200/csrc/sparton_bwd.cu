@@ -150,21 +150,37 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   }
 
   // Stage (I, g) of local batch rows [lb0, lb0 + DE_BC) into buffer `buf`.
-  auto stage_gi = [&](int lb0, int buf) {
-    for (int e = threadIdx.x; e < DE_BC * DE_VB; e += DE_THREADS) {
+  // (I, g) staging is register double-buffered: the raw (Y, dY, I) of the tile
+  // after next are loaded right after a tile boundary and only consumed at the
+  // next boundary, so their latency never stalls the gather pipeline.
+  constexpr int GI_PER_THREAD = DE_BC * DE_VB / DE_THREADS;
+  float ry[GI_PER_THREAD], rdy[GI_PER_THREAD];
+  int ri[GI_PER_THREAD];
+  auto load_gi = [&](int lb0) {
+#pragma unroll
+    for (int q = 0; q < GI_PER_THREAD; ++q) {
+      const int e = threadIdx.x + q * DE_THREADS;
       const int bb = e / DE_VB, vv = e % DE_VB;
       const int lb = lb0 + bb, v = v0 + vv;
-      float g = 0.f;
-      int idx = -1;
+      ry[q] = 0.f;
+      rdy[q] = 0.f;
+      ri[q] = -1;
       if (lb < nb && v < p.V) {
         const size_t b = (size_t)(bbeg + lb);
-        const float y = p.Y[b * p.ldY + v];
-        if (y > 0.f) {
-          g = pair_grad(y, p.dY[b * p.ldDY + v]);
-          idx = p.I[b * p.ldY + v];
-        }
+        ry[q] = p.Y[b * p.ldY + v];
+        rdy[q] = p.dY[b * p.ldDY + v];
+        ri[q] = p.I[b * p.ldY + v];
       }
-      gi_s[(buf * DE_BC + bb) * DE_VB + vv] = make_int2(idx, __float_as_int(g));
+    }
+  };
+  auto store_gi = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < GI_PER_THREAD; ++q) {
+      const int e = threadIdx.x + q * DE_THREADS;
+      const int bb = e / DE_VB, vv = e % DE_VB;
+      const bool act = ry[q] > 0.f;
+      gi_s[(buf * DE_BC + bb) * DE_VB + vv] =
+          make_int2(act ? ri[q] : -1, __float_as_int(act ? pair_grad(ry[q], rdy[q]) : 0.f));
     }
   };
   // Lanes 0..DE_RPW-1 gather this warp's rows for local batch row lb into ring
@@ -215,8 +231,13 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   }
 
   const int ntiles = (nb + DE_BC - 1) / DE_BC;
-  stage_gi(0, 0);
-  if (ntiles > 1) stage_gi(DE_BC, 1);
+  load_gi(0);
+  store_gi(0);
+  if (ntiles > 1) {
+    load_gi(DE_BC);
+    store_gi(1);
+  }
+  if (ntiles > 2) load_gi(2 * DE_BC);
   __syncthreads();
   // Prologue: NST-1 batch rows in flight (all within tiles 0/1, NST-1 < DE_BC).
   for (int lb = 0; lb < C::NST - 1 && lb < nb; ++lb) issue(lb);
@@ -228,7 +249,8 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
       // Tile t is resident (staged one tile ahead); refill the other buffer with
       // tile t+1 once every warp is done with tile t-1.
       __syncthreads();
-      if (t + 1 < ntiles) stage_gi((t + 1) * DE_BC, buf ^ 1);
+      if (t + 1 < ntiles) store_gi(buf ^ 1);        // loaded one tile ago
+      if (t + 2 < ntiles) load_gi((t + 2) * DE_BC);
       __syncthreads();
     }
     // Issue local batch row lb+NST-1: its tile is t or t+1 (NST-1 < DE_BC), both resident.

@@ -171,8 +171,12 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
-      const uint64_t pol_e = p.e_evict_last ? ptx::policy_evict_last() : ptx::policy_evict_normal();
-      const uint64_t pol_h = ptx::policy_evict_normal();
+      // L2 policies: 0 evict_normal, 1 evict_last, 2 evict_first (experiment switch)
+      auto pol = [](int k) {
+        return k == 1 ? ptx::policy_evict_last() : (k == 2 ? ptx::policy_evict_first() : ptx::policy_evict_normal());
+      };
+      const uint64_t pol_e = pol(p.e_evict_last & 3);
+      const uint64_t pol_h = pol((p.e_evict_last >> 2) & 3);
       int st = 0;
       uint32_t ph = 0;
       UnitIter it((int)cluster, (int)nclusters);
@@ -286,7 +290,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         __syncwarp();
         if (lane == 0) {
           const uint32_t te = acc ? tempty1 : tempty0;
-          if constexpr (CG == 2) ptx::mbar_arrive_cluster(te);
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster_relaxed(te);
           else ptx::mbar_arrive(te);
         }
         acc ^= 1;
