@@ -109,7 +109,7 @@ template <int CPL>
 struct DeCfg {
   static constexpr int DS = 256 * CPL;                       // slice width (elements)
   static constexpr int ROW_BYTES = DS * 2;
-  static constexpr int NST = CPL >= 3 ? 4 : (CPL == 2 ? 6 : 8);
+  static constexpr int NST = CPL >= 2 ? 4 : 8;
   static constexpr int WARP_STAGE_BYTES = DE_RPW * ROW_BYTES;  // DE_RPW rows per warp per stage
   static constexpr int RING_BYTES = DE_WARPS * NST * WARP_STAGE_BYTES;
   static constexpr int GI_BYTES = 2 * DE_BC * DE_VB * 8;      // (I, g) pairs, double buffered
@@ -243,9 +243,13 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   for (int lb = 0; lb < C::NST - 1 && lb < nb; ++lb) issue(lb);
   const uint8_t* lane_src = ring + lane * 16;
 
-  for (int lb = 0; lb < nb; ++lb) {
-    const int t = lb / DE_BC, bb = lb - t * DE_BC, buf = t & 1;
-    if (bb == 0 && t > 0) {
+  // Main loop, unrolled by NST so every ring stage index and phase is a
+  // compile-time constant (DE_BC is a multiple of NST: tile boundaries fall on
+  // iteration boundaries).
+  static_assert(DE_BC % C::NST == 0, "tile must hold whole pipeline rounds");
+  for (int lb0 = 0; lb0 < nb; lb0 += C::NST) {
+    const int t = lb0 / DE_BC, buf = t & 1;
+    if (lb0 % DE_BC == 0 && t > 0) {
       // Tile t is resident (staged one tile ahead); refill the other buffer with
       // tile t+1 once every warp is done with tile t-1.
       __syncthreads();
@@ -253,27 +257,34 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
       if (t + 2 < ntiles) load_gi((t + 2) * DE_BC);
       __syncthreads();
     }
-    // Issue local batch row lb+NST-1: its tile is t or t+1 (NST-1 < DE_BC), both resident.
-    if (lb + C::NST - 1 < nb) issue(lb + C::NST - 1);
-    const int st = lb % C::NST;
-    float g[DE_RPW];
+    const uint32_t parity = (uint32_t)(lb0 / C::NST) & 1u;
+    const int2* gi_row = gi_s + (buf * DE_BC + (lb0 - t * DE_BC)) * DE_VB + warp;
 #pragma unroll
-    for (int r = 0; r < DE_RPW; ++r) g[r] = __int_as_float(gi_s[(buf * DE_BC + bb) * DE_VB + warp + DE_WARPS * r].y);
-    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (lb / C::NST) & 1);
-    const uint8_t* src = lane_src + st * C::WARP_STAGE_BYTES;
+    for (int j = 0; j < C::NST; ++j) {
+      const int lb = lb0 + j;
+      if (lb < nb) {
+        // Issue batch row lb+NST-1 (tile t or t+1, both resident) into stage (j-1) mod NST.
+        if (lb + C::NST - 1 < nb) issue(lb + C::NST - 1);
+        float g[DE_RPW];
 #pragma unroll
-    for (int r = 0; r < DE_RPW; ++r) {
-      gsum[r] += g[r];
-      const uint64_t gg = pack_gg(g[r]);
+        for (int r = 0; r < DE_RPW; ++r) g[r] = __int_as_float(gi_row[j * DE_VB + DE_WARPS * r].y);
+        ptx::mbar_wait(ptx::smem_u32(&bars[j]), parity);
+        const uint8_t* src = lane_src + j * C::WARP_STAGE_BYTES;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        if (dvalid[c]) {
-          const int4 x = *reinterpret_cast<const int4*>(src + r * C::ROW_BYTES + c * 512);
-          fma8(&acc[r][c * 8], gg, x);
+        for (int r = 0; r < DE_RPW; ++r) {
+          gsum[r] += g[r];
+          const uint64_t gg = pack_gg(g[r]);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            if (dvalid[c]) {
+              const int4 x = *reinterpret_cast<const int4*>(src + r * C::ROW_BYTES + c * 512);
+              fma8(&acc[r][c * 8], gg, x);
+            }
+          }
         }
+        __syncwarp();
       }
     }
-    __syncwarp();
   }
 
 #pragma unroll
