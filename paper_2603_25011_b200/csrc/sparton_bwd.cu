@@ -29,6 +29,7 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 
 #include "ptx.cuh"
 #include "sparton_internal.h"
@@ -37,10 +38,7 @@ namespace sparton {
 
 namespace {
 
-constexpr int DE_VB = 32;       // vocab rows per CTA
-constexpr int DE_RPW = 2;       // vocab rows per warp
-constexpr int DE_WARPS = DE_VB / DE_RPW;
-constexpr int DE_THREADS = DE_WARPS * 32;
+constexpr int DE_RPW = 2;       // vocab rows per warp (a CTA of W warps owns 2*W vocab rows)
 constexpr int DH_THREADS = 256;
 
 __device__ __forceinline__ float pair_grad(float y, float dy) {
@@ -105,8 +103,11 @@ __device__ __forceinline__ void store8<__nv_bfloat16>(__nv_bfloat16* dst, const 
 // staged in smem (double buffered, one __syncthreads per 32 batch rows).
 constexpr int DE_BC = 32;       // batch rows per (g, I) tile
 
-template <int CPL>
+template <int CPL, int W>
 struct DeCfg {
+  static constexpr int DE_WARPS = W;
+  static constexpr int DE_VB = W * DE_RPW;
+  static constexpr int DE_THREADS = W * 32;
   static constexpr int DS = 256 * CPL;                       // slice width (elements)
   static constexpr int ROW_BYTES = DS * 2;
   static constexpr int NST = CPL >= 2 ? 4 : 8;
@@ -122,10 +123,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
-template <int CPL, bool FULL, typename OutT>
-__global__ void __launch_bounds__(DE_THREADS, 1)
+template <int CPL, int W, bool FULL, typename OutT>
+__global__ void __launch_bounds__(W * 32, 1)
 sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
-  using C = DeCfg<CPL>;
+  using C = DeCfg<CPL, W>;
+  constexpr int DE_WARPS = C::DE_WARPS;
+  constexpr int DE_VB = C::DE_VB;
+  constexpr int DE_THREADS = C::DE_THREADS;
   extern __shared__ __align__(128) uint8_t de_smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -554,29 +558,58 @@ int route_nseg(int S) {
 }
 size_t route_smem_bytes(int S, int nseg) { return (size_t)RT_WIN * 8 + ((size_t)nseg * S + 32) * 4; }
 
-template <int CPL, bool FULL, typename OutT>
+template <int CPL, int W, bool FULL, typename OutT>
 int launch_de(const BwdParams& p, cudaStream_t stream) {
-  constexpr int smem = DeCfg<CPL>::SMEM_BYTES;
-  cudaError_t e = cudaFuncSetAttribute(sparton_bwd_de_kernel<CPL, FULL, OutT>,
+  using C = DeCfg<CPL, W>;
+  constexpr int smem = C::SMEM_BYTES;
+  cudaError_t e = cudaFuncSetAttribute(sparton_bwd_de_kernel<CPL, W, FULL, OutT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de)", e);
-  dim3 grid((p.V + DE_VB - 1) / DE_VB, (p.D + 256 * CPL - 1) / (256 * CPL));
+  dim3 grid((p.V + C::DE_VB - 1) / C::DE_VB, (p.D + 256 * CPL - 1) / (256 * CPL));
   for (int b0 = 0; b0 < p.B; b0 += p.bchunk) {
-    sparton_bwd_de_kernel<CPL, FULL, OutT><<<grid, DE_THREADS, smem, stream>>>(p, b0, min(p.B, b0 + p.bchunk));
+    sparton_bwd_de_kernel<CPL, W, FULL, OutT><<<grid, C::DE_THREADS, smem, stream>>>(p, b0, min(p.B, b0 + p.bchunk));
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_de_kernel", e);
   }
   return SPARTON_OK;
 }
 
-template <int CPL, typename OutT>
-int launch_bwd_t(const BwdParams& p, cudaStream_t stream) {
-  const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
-  {
-    const int rc = (p.D % (256 * CPL) == 0) ? launch_de<CPL, true, OutT>(p, stream)
-                                             : launch_de<CPL, false, OutT>(p, stream);
-    if (rc != SPARTON_OK) return rc;
+// Per-device side stream + fork/join events: dE (independent of the route)
+// runs concurrently with route -> dH so the two L2-gather-bound kernels share
+// the SMs (an 8-warp dE CTA with a 104 KB ring leaves room for two dH CTAs).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+int side_stream(SideStream& out) {
+  static std::mutex mu;
+  static SideStream cache[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error("cudaGetDevice", e);
+  if (dev >= 64) return set_error(SPARTON_ENOTSUP, "device index >= 64");
+  std::lock_guard<std::mutex> lk(mu);
+  SideStream& c = cache[dev];
+  if (!c.s) {
+    if ((e = cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming)) != cudaSuccess)
+      return set_cuda_error("side stream setup", e);
   }
+  out = c;
+  return SPARTON_OK;
+}
+
+template <int CPL, int W, typename OutT>
+int launch_de_any(const BwdParams& p, cudaStream_t stream) {
+  return (p.D % (256 * CPL) == 0) ? launch_de<CPL, W, true, OutT>(p, stream)
+                                  : launch_de<CPL, W, false, OutT>(p, stream);
+}
+
+template <int CPL, typename OutT>
+int launch_route_dh(const BwdParams& p, cudaStream_t stream) {
+  const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
   {
     const int nseg = route_nseg(p.S);
     const size_t smem = route_smem_bytes(p.S, nseg);
@@ -598,6 +631,30 @@ int launch_bwd_t(const BwdParams& p, cudaStream_t stream) {
       if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
     }
   }
+  return SPARTON_OK;
+}
+
+template <int CPL, typename OutT>
+int launch_bwd_t(const BwdParams& p, cudaStream_t stream) {
+  int mode = 1;
+  if (const char* ev = getenv("SPARTON_BWD_CONCURRENT")) mode = atoi(ev);
+  if (mode == 0) {
+    const int rc = launch_de_any<CPL, 16, OutT>(p, stream);
+    if (rc != SPARTON_OK) return rc;
+    return launch_route_dh<CPL, OutT>(p, stream);
+  }
+  SideStream ss;
+  int rc = side_stream(ss);
+  if (rc != SPARTON_OK) return rc;
+  cudaError_t e = cudaEventRecord(ss.fork, stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.s, ss.fork, 0);
+  if (e != cudaSuccess) return set_cuda_error("fork side stream", e);
+  rc = (mode == 2) ? launch_de_any<CPL, 16, OutT>(p, ss.s) : launch_de_any<CPL, 8, OutT>(p, ss.s);
+  if (rc != SPARTON_OK) return rc;
+  if ((e = cudaEventRecord(ss.join, ss.s)) != cudaSuccess) return set_cuda_error("record join", e);
+  rc = launch_route_dh<CPL, OutT>(p, stream);
+  if (rc != SPARTON_OK) return rc;
+  if ((e = cudaStreamWaitEvent(stream, ss.join, 0)) != cudaSuccess) return set_cuda_error("join side stream", e);
   return SPARTON_OK;
 }
 
