@@ -73,7 +73,9 @@ SPARTON_API int sparton_device_sm_count(void);
  *   H     : bf16 [B*S, D]       E    : bf16 [V, D]
  *   bias  : f32 [V]             mask : u8 [B*S] (row-major B x S)
  *   Y     : f32 [B, ldY]        I    : i32 [B, ldY]
- *   cta_group : 0 = auto, 1 = single-CTA UMMA (M=128), 2 = CTA pair (M=256)
+ *   cta_group : CTAs per cluster: 0 = auto (2), 1 = single-CTA UMMA (M=128),
+ *               2 = CTA pair (cta_group::2, M=256), 4 = two CTA pairs sharing
+ *               each H tile through TMA multicast (halves H L2 traffic)
  */
 SPARTON_API int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* mask,
                 float* Y, int32_t* I,

@@ -136,6 +136,19 @@ __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t d
       : "memory");
 }
 
+// CTA-pair variant with cluster multicast: the box lands at the same smem
+// offset in every CTA of `mask`; each destination's bytes are signalled on the
+// barrier of its pair leader (peer bit cleared).
+__device__ __forceinline__ void tma_load_2d_cg2_mc(const CUtensorMap* m, uint32_t dst, uint32_t bar,
+                                                   int32_t c0, int32_t c1, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5, %6;"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask),
+         "l"(policy)
+      : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));

@@ -158,14 +158,23 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
   if (!H || !E || !bias || !mask || !Y || !I) return set_error(SPARTON_EINVAL, "null pointer argument");
   if (!aligned16(H) || !aligned16(E)) return set_error(SPARTON_EINVAL, "H and E must be 16-byte aligned");
   if (ldY < V) return set_error(SPARTON_EINVAL, "ldY must be >= V");
-  if (cta_group < 0 || cta_group > 2) return set_error(SPARTON_EINVAL, "cta_group must be 0, 1 or 2");
+  if (cta_group != 0 && cta_group != 1 && cta_group != 2 && cta_group != 4)
+    return set_error(SPARTON_EINVAL, "cta_group must be 0, 1, 2 or 4");
   if ((rc = check_device())) return rc;
   DevInfo d;
   device_info(d);
-  const int cg = cta_group == 0 ? 2 : cta_group;
+  int cg = cta_group;
+  if (cg == 0) {
+    // Default: one CTA pair per cluster.  Two pairs sharing H tiles by TMA
+    // multicast (cg = 4) cut L2 traffic by ~30 % but ran 1.6x slower at cfg3
+    // (lock-step coupling of the pairs, 4-CTA clusters leave SMs idle).
+    cg = 2;
+    if (const char* ev = getenv("SPARTON_FWD_CLUSTER")) cg = atoi(ev);
+    if (cg != 1 && cg != 2 && cg != 4) cg = 2;
+  }
   CUtensorMap tmE, tmH;
   if ((rc = encode_bf16_2d(&tmE, E, V, D, 128, 64))) return rc;
-  if ((rc = encode_bf16_2d(&tmH, H, B * S, D, 256 / cg, 64))) return rc;
+  if ((rc = encode_bf16_2d(&tmH, H, B * S, D, fwd_h_box_rows(cg), 64))) return rc;
   FwdParams prm = {};
   prm.bias = bias;
   prm.mask = mask;

@@ -35,12 +35,13 @@
 
 namespace sparton {
 
-template <int CG>
+template <int CG, int NP = 1>
 struct FwdCfg {
   static constexpr int BM = 128;                 // vocab rows per CTA (TMEM lanes)
-  static constexpr int TILE_V = BM * CG;         // vocab rows per unit
+  static constexpr int TILE_V = BM * CG * NP;    // vocab rows per unit (NP pairs share H tiles)
   static constexpr int SN = 256;                 // sequence positions per chunk (UMMA N)
-  static constexpr int BN_CTA = SN / CG;         // H rows each CTA loads per chunk
+  static constexpr int BN_CTA = SN / CG;         // H rows each CTA holds per chunk
+  static constexpr int BN_LOAD = BN_CTA / NP;    // H rows each CTA loads (and multicasts to NP CTAs)
   static constexpr int BK = 64;                  // K per stage = one 128-B swizzle row
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN_CTA * BK * 2;
@@ -124,11 +125,12 @@ __device__ __forceinline__ void reduce_group(const float (&r)[32], float bias, u
   }
 }
 
-template <int CG>
-__global__ void __launch_bounds__(FwdCfg<CG>::NUM_THREADS, 1)
+template <int CG, int NP>
+__global__ void __launch_bounds__(FwdCfg<CG, NP>::NUM_THREADS, 1)
 sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmH,
                    const FwdParams p) {
-  using C = FwdCfg<CG>;
+  using C = FwdCfg<CG, NP>;
+  static_assert(NP == 1 || CG == 2, "H multicast across pairs needs CTA pairs");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128-B swizzle atoms.
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -142,7 +144,11 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
+  const uint32_t crank = (CG == 2) ? ptx::cluster_ctarank() : 0;   // rank in the cluster
+  const uint32_t rank = crank & (CG - 1);                            // rank in the CTA pair
+  const uint32_t pair = crank / CG;                                  // pair index in the cluster
+  const uint16_t pair_mask = (uint16_t)(((1u << CG) - 1u) << (pair * CG));
+  constexpr uint16_t all_mask = (uint16_t)((1u << (CG * NP)) - 1u);
   const long long cluster = (CG == 2) ? (long long)ptx::cluster_id_x() : (long long)blockIdx.x;
   const long long nclusters = (CG == 2) ? (long long)ptx::nclusters_x() : (long long)gridDim.x;
 
@@ -151,7 +157,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     ptx::prefetch_tmap(&tmH);
     for (int i = 0; i < C::NST; ++i) {
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&empty[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), NP);   // one MMA commit per pair (multicast H)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&tfull[i]), 1);
@@ -182,9 +188,9 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       UnitIter it((int)cluster, (int)nclusters);
       int b, vt;
       while (it.next(p, b, vt)) {
-        const int vrow = vt * C::TILE_V + (int)rank * C::BM;
+        const int vrow = vt * C::TILE_V + (int)pair * (C::BM * CG) + (int)rank * C::BM;
         for (int sc = 0; sc < nsc; ++sc) {
-          const int hrow = b * p.S + sc * C::SN + (int)rank * C::BN_CTA;
+          const int hrow = b * p.S + sc * C::SN + (int)rank * C::BN_CTA + (int)pair * C::BN_LOAD;
           for (int kb = 0; kb < nkb; ++kb) {
             ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
             const uint32_t sa = ptx::smem_u32(stage_base + st * C::STAGE_BYTES);
@@ -197,7 +203,15 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
             } else {
               if (rank == 0) ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES * 2);
               ptx::tma_load_2d_cg2(&tmE, sa, fb, kb * C::BK, vrow, pol_e);
-              ptx::tma_load_2d_cg2(&tmH, sb, fb, kb * C::BK, hrow, pol_h);
+              if constexpr (NP == 1) {
+                ptx::tma_load_2d_cg2(&tmH, sb, fb, kb * C::BK, hrow, pol_h);
+              } else {
+                // Same H rows are needed by CTA `rank` of every pair: each loads
+                // 1/NP of them and multicasts to its counterparts.
+                const uint16_t mc = (uint16_t)(0x5555u << rank) & all_mask;   // cluster ranks rank, rank+2, ...
+                ptx::tma_load_2d_cg2_mc(&tmH, sb + pair * (C::BN_LOAD * C::BK * 2), fb, kb * C::BK, hrow, mc,
+                                        pol_h);
+              }
             }
             if (++st == C::NST) { st = 0; ph ^= 1; }
           }
@@ -230,10 +244,11 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
               // +32 bytes along K inside the 128-B swizzle row = +2 in the >>4 address field.
               ptx::umma_bf16<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
             }
-            ptx::umma_commit<CG>(ptx::smem_u32(&empty[st]));
+            // The stage's H half was written by every pair's producer: release it cluster-wide.
+            ptx::umma_commit<CG>(ptx::smem_u32(&empty[st]), all_mask);
             if (++st == C::NST) { st = 0; ph ^= 1; }
           }
-          ptx::umma_commit<CG>(ptx::smem_u32(&tfull[acc]));
+          ptx::umma_commit<CG>(ptx::smem_u32(&tfull[acc]), pair_mask);
           acc ^= 1;
           if (acc == 0) aph ^= 1;
         }
@@ -247,15 +262,15 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     uint32_t tempty0 = ptx::smem_u32(&tempty[0]);
     uint32_t tempty1 = ptx::smem_u32(&tempty[1]);
     if constexpr (CG == 2) {
-      tempty0 = ptx::mapa(tempty0, 0);
-      tempty1 = ptx::mapa(tempty1, 0);
+      tempty0 = ptx::mapa(tempty0, pair * CG);
+      tempty1 = ptx::mapa(tempty1, pair * CG);
     }
     int acc = 0;
     uint32_t aph = 0;
     UnitIter it((int)cluster, (int)nclusters);
     int b, vt;
     while (it.next(p, b, vt)) {
-      const int v = vt * C::TILE_V + (int)rank * C::BM + row;
+      const int v = vt * C::TILE_V + (int)pair * (C::BM * CG) + (int)rank * C::BM + row;
       const float bv = (v < p.V) ? __ldg(p.bias + v) : 0.0f;
       const uint8_t* mrow = p.mask + (size_t)b * p.S;
       float best = -INFINITY;
@@ -324,18 +339,18 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
 
 // ------------------------------------------------------------------ host side
 
-template <int CG>
+template <int CG, int NP>
 int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdParams& prm,
                     int num_sms, cudaStream_t stream) {
-  using C = FwdCfg<CG>;
-  auto kern = sparton_fwd_kernel<CG>;
+  using C = FwdCfg<CG, NP>;
+  constexpr int CL = CG * NP;   // cluster size
+  auto kern = sparton_fwd_kernel<CG, NP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(fwd)", e);
   long long want = prm.num_units;
-  int grid = num_sms;                    // persistent: one CTA per SM
-  if (CG == 2) grid = (num_sms / 2) * 2;
-  if (want < grid / CG) grid = (int)want * CG;
-  if (grid < CG) grid = CG;
+  int grid = (num_sms / CL) * CL;        // persistent: one CTA per SM, whole clusters
+  if (want < grid / CL) grid = (int)want * CL;
+  if (grid < CL) grid = CL;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
@@ -345,7 +360,7 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
   int na = 0;
   if (CG == 2) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     na = 1;
@@ -359,12 +374,12 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
 
 static int gcd_int(int a, int b) { while (b) { const int t = a % b; a = b; b = t; } return a; }
 
-int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cta_group,
+int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cluster_ctas,
                int num_sms, cudaStream_t stream) {
-  const int tile_v = 128 * cta_group;
+  const int tile_v = 128 * cluster_ctas;
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
   prm.num_units = (long long)prm.num_vt * prm.B;
-  const int nclusters = max(1, num_sms / cta_group);
+  const int nclusters = max(1, num_sms / cluster_ctas);
   // E group of ~48 MB stays L2-resident while H streams (see UnitIter).
   const long long tile_bytes = (long long)tile_v * prm.D * 2;
   long long group_bytes = 24ll << 20;
@@ -379,12 +394,16 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   if (rot < 1) rot = 1;
   while (gcd_int(rot, nclusters) != 1) ++rot;
   prm.rot = rot % nclusters;
-  if (cta_group == 2) return launch_fwd_impl<2>(tmE, tmH, prm, num_sms, stream);
-  return launch_fwd_impl<1>(tmE, tmH, prm, num_sms, stream);
+  if (cluster_ctas == 4) return launch_fwd_impl<2, 2>(tmE, tmH, prm, num_sms, stream);
+  if (cluster_ctas == 2) return launch_fwd_impl<2, 1>(tmE, tmH, prm, num_sms, stream);
+  return launch_fwd_impl<1, 1>(tmE, tmH, prm, num_sms, stream);
 }
 
-int fwd_smem_bytes(int cta_group) {
-  return cta_group == 2 ? FwdCfg<2>::SMEM_BYTES : FwdCfg<1>::SMEM_BYTES;
+// Rows of H each CTA loads per TMA box for a cluster of `cluster_ctas` CTAs.
+int fwd_h_box_rows(int cluster_ctas) { return 256 / cluster_ctas; }
+
+int fwd_smem_bytes(int cluster_ctas) {
+  return cluster_ctas >= 2 ? FwdCfg<2>::SMEM_BYTES : FwdCfg<1>::SMEM_BYTES;
 }
 
 }  // namespace sparton

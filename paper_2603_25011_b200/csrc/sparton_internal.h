@@ -61,9 +61,10 @@ BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long lo
 int set_error(int code, const char* msg);
 int set_cuda_error(const char* what, cudaError_t e);
 
-int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cta_group,
+int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cluster_ctas,
                int num_sms, cudaStream_t stream);
-int fwd_smem_bytes(int cta_group);
+int fwd_smem_bytes(int cluster_ctas);
+int fwd_h_box_rows(int cluster_ctas);
 int launch_bwd(const BwdParams& prm, int grad_dtype, cudaStream_t stream);
 int bwd_max_seq();
 

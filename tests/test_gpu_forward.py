@@ -48,7 +48,7 @@ def assert_parity(H, E, b, mask, Yg, Ig, Yr, Ir):
 # ---------------------------------------------------------------- golden fixtures (reference outputs)
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("cg", [1, 2, 4])
 def test_golden_forward(cuda_device, name, cg):
     g = load_golden(name)
     H, E, b, m = g["H"], g["E"], g["b"], g["mask"]
@@ -153,17 +153,19 @@ def test_grid_vs_oracle(cuda_device, dims, keep):
     H, E, b, m = orc.seeded_inputs(B, S, D, V, 1000 + B * 7 + S + V, mask_keep=keep)
     Hr, Er = orc.bf16_round(H), orc.bf16_round(E)
     Yr, Ir = orc.forward(Hr, Er, b, m)
-    for cg in (1, 2):
+    for cg in (1, 2, 4):
         Yg, Ig = run_fwd(Hr, Er, b, m, cta_group=cg)
         assert_parity(Hr, Er, b, m, Yg, Ig, Yr, Ir)
 
 
 def test_cta_group_variants_bitwise_equal(cuda_device):
+    # single CTA, CTA pair and two pairs sharing H by multicast: same per-element math
     H, E, b, m = orc.seeded_inputs(3, 300, 768, 1000, 77, mask_keep=0.9)
     Y1, I1 = run_fwd(H, E, b, m, cta_group=1)
-    Y2, I2 = run_fwd(H, E, b, m, cta_group=2)
-    assert Y1.tobytes() == Y2.tobytes()
-    assert np.array_equal(I1, I2)
+    for cg in (2, 4):
+        Y2, I2 = run_fwd(H, E, b, m, cta_group=cg)
+        assert Y1.tobytes() == Y2.tobytes()
+        assert np.array_equal(I1, I2)
 
 
 def test_every_output_written_once(cuda_device):
