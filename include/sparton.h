@@ -83,9 +83,11 @@ SPARTON_API int sparton_fwd(const void* H, const void* E, const float* bias, con
                 int cta_group, void* stream);
 
 /* Workspace bytes sparton_bwd needs for these sizes: the argmax-routed (v, g)
- * pair lists for dH (B*V*8 bytes), their offsets and per-row cursors, plus an
- * fp32 dH accumulator (B*S*D*4) when grad_dtype is bf16 and the vocabulary is
- * processed in more than one L2-sized chunk.  Pure host arithmetic. */
+ * pair lists for dH (B*V*8 bytes) and their offsets, the per-(b, v) (s, g)
+ * records of the staged dE (B*V*8 bytes, S <= 856), plus an fp32 dH
+ * accumulator (B*S*D*4) when grad_dtype is bf16 and the vocabulary is
+ * processed in more than one L2-sized chunk (and, for S > 856, an fp32 dE
+ * carry for the gathered dE's batch-chunk passes).  Pure host arithmetic. */
 SPARTON_API size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t D, int64_t V,
                                                int grad_dtype);
 

@@ -63,8 +63,8 @@ int device_info(DevInfo& out) {
   return SPARTON_OK;
 }
 
-int encode_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols,
-                   int box_rows, int box_cols) {
+int encode_bf16_2d_swz(CUtensorMap* map, const void* ptr, long long rows, long long cols,
+                       int box_rows, int box_cols, CUtensorMapSwizzle swz) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return set_error(SPARTON_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -72,7 +72,7 @@ int encode_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long 
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[160];
@@ -83,9 +83,19 @@ int encode_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long 
   return SPARTON_OK;
 }
 
+int encode_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols,
+                   int box_rows, int box_cols) {
+  return encode_bf16_2d_swz(map, ptr, rows, cols, box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
+
+int encode_bf16_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long long cols, int box_rows,
+                         int box_cols) {
+  return encode_bf16_2d_swz(map, ptr, rows, cols, box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
 
 int set_error(int code, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -172,6 +182,11 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
     if (const char* ev = getenv("SPARTON_FWD_CLUSTER")) cg = atoi(ev);
     if (cg != 1 && cg != 2 && cg != 4) cg = 2;
   }
+  if (const char* ev = getenv("SPARTON_L2_PERSIST_MB")) {
+    // Experiment switch: L2 set-aside for evict_last (persisting) lines.
+    static std::once_flag once;
+    std::call_once(once, [ev]() { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(ev) << 20); });
+  }
   CUtensorMap tmE, tmH;
   if ((rc = encode_bf16_2d(&tmE, E, V, D, 128, 64))) return rc;
   if ((rc = encode_bf16_2d(&tmH, H, B * S, D, fwd_h_box_rows(cg), 64))) return rc;
@@ -187,7 +202,9 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
   prm.ldY = ldY;
   {
     const char* ev = getenv("SPARTON_E_EVICT_LAST");
-    prm.e_evict_last = ev ? atoi(ev) : 1;   // bits 0-1: E policy, bits 2-3: H policy
+    // bits 0-1: E policy, bits 2-3: H policy (0 normal, 1 evict_last, 2 evict_first).
+    // Both evict_last measured lowest DRAM traffic (profiles/r01_fwd_l2_policy.txt).
+    prm.e_evict_last = ev ? atoi(ev) : 5;
   }
   return launch_fwd(tmE, tmH, prm, cg, d.sms, static_cast<cudaStream_t>(stream));
 }
@@ -249,7 +266,13 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
   p.nwin = ws.nwin;
   p.wpc = ws.wpc;
   p.nchunks = ws.nchunks;
-  return launch_bwd(p, grad_dtype, static_cast<cudaStream_t>(stream));
+  p.gi = ws.de_staged ? reinterpret_cast<int2*>(wsb + ws.gi) : nullptr;
+  p.ldGI = ws.ldGI;
+  CUtensorMap tmH;
+  if (ws.de_staged) {
+    if ((rc = encode_bf16_2d_plain(&tmH, H, B * S, D, de_staged_rows((int)S), 64))) return rc;
+  }
+  return launch_bwd(p, ws.de_staged ? &tmH : nullptr, grad_dtype, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

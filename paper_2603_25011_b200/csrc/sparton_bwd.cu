@@ -11,7 +11,13 @@
 // every output element has exactly one owner that accumulates in the
 // reference's order — b ascending for dE/db, v ascending for dH.
 //
-//   K2 sparton_bwd_de_kernel  : CTA owns 32 vocab rows x one D slice; warps own
+//   K2s sparton_bwd_de_staged_kernel (S <= 856, the default): CTA owns 748
+//                               vocab rows x 64 columns of D with fp32 sums in
+//                               registers over the whole batch; per batch row
+//                               the H[b] slice is staged in smem (TMA multicast
+//                               over a 4-CTA cluster) and every pair reads its
+//                               argmax row from smem.  db by a column-sum kernel.
+//   K2 sparton_bwd_de_kernel  : (S > 856) CTA owns 32 vocab rows x one D slice; warps own
 //                               4 vocab rows, lanes 8-wide D chunks; for each
 //                               batch row (ascending) each warp gathers its
 //                               argmax H rows with 1-D TMA bulk copies into a
@@ -312,6 +318,151 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
   }
 }
 
+// ------------------------------------------------------------------ K2s: staged dE
+// dE with on-chip reuse of H instead of per-pair L2 gathers.  A CTA owns a
+// block of VB vocab rows x one 64-column slice of D and keeps the VB x 64 fp32
+// accumulators in registers for the whole batch (no carry passes).  For each
+// batch row b (ascending — the reference's order) the slice H[b, 0:S, d0:d0+64]
+// is staged in shared memory (S rows of 128 B) together with the block's
+// (s, g) records; every (b, v) pair then reads its argmax row from shared
+// memory.  Eight lanes own one vocab row (16 B = 8 columns each), so a warp's
+// 128-bit shared load touches four whole 128-B rows: conflict-free for any
+// argmax pattern.  The cluster's DEST_CL CTAs hold neighbouring vocab blocks
+// of the same slice: each loads S/DEST_CL rows of the tile and multicasts them
+// to all, so a tile costs one L2 read per cluster.  Warp NW is the TMA
+// producer; stage reuse is released cluster-wide (every consumer warp arrives
+// on the empty barrier of every CTA, since peers' multicasts write into it).
+constexpr int DEST_CL = 4;
+constexpr int DEST_DD = 64;
+
+template <int NW, int J>
+struct DeStCfg {
+  static constexpr int THREADS = (NW + 1) * 32;
+  static constexpr int GROUPS = NW * 4;       // 8-lane groups, one vocab row each per step
+  static constexpr int VB = GROUPS * J;       // vocab rows per CTA
+  static constexpr int GI_BYTES = VB * 8;
+};
+
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* m, uint32_t dst, uint32_t bar, int32_t c0,
+                                               int32_t c1, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5, %6;"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
+
+template <int NW, int J, typename OutT>
+__global__ void __launch_bounds__(DeStCfg<NW, J>::THREADS, 1)
+sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdParams p, int R, int nst,
+                             int stage_bytes) {
+  using C = DeStCfg<NW, J>;
+  extern __shared__ __align__(128) uint8_t ds_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ds_smem + (size_t)nst * stage_bytes);
+  uint64_t* empty = full + nst;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = ptx::cluster_ctarank();
+  const int v0 = blockIdx.x * C::VB;
+  const int d0 = blockIdx.y * DEST_DD;
+  // Stage layout: [zero row][S-row tile][GI records].  s = -1 (inactive pair)
+  // addresses the zero row, so inactive pairs never touch H.
+  const uint32_t tile_bytes = (uint32_t)(DEST_CL * R * 128);
+  const uint32_t gi_off = 128 + tile_bytes;
+
+  // Zero rows and GI regions start zeroed / (-1, 0): entries past the
+  // vocabulary (never copied) read the zero row with g = 0.
+  for (int i = threadIdx.x; i < nst * 8; i += C::THREADS)
+    reinterpret_cast<int4*>(ds_smem + (size_t)(i / 8) * stage_bytes)[i % 8] = make_int4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < nst * C::GI_BYTES / 16; i += C::THREADS) {
+    const int st = i / (C::GI_BYTES / 16), o = i % (C::GI_BYTES / 16);
+    reinterpret_cast<int4*>(ds_smem + (size_t)st * stage_bytes + gi_off)[o] = make_int4(-1, 0, -1, 0);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), DEST_CL * NW);
+    }
+    ptx::fence_mbar_init();
+  }
+  ptx::fence_proxy_async();   // zeroed GI visible to the async proxy before any bulk copy lands
+  ptx::cluster_sync();
+
+  if (warp == NW) {
+    if (lane == 0) {
+      // ------------------------------------------------ producer
+      const uint64_t pol = ptx::policy_evict_normal();
+      const long long vrem = (long long)p.ldGI - v0;          // even
+      const uint32_t gi_bytes = (uint32_t)(vrem >= C::VB ? C::GI_BYTES : (vrem > 0 ? vrem * 8 : 0));
+      int st = 0;
+      uint32_t ph = 0;
+      for (int b = 0; b < p.B; ++b) {
+        ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
+        const uint32_t sbase = ptx::smem_u32(ds_smem + (size_t)st * stage_bytes);
+        const uint32_t fb = ptx::smem_u32(&full[st]);
+        ptx::mbar_arrive_expect_tx(fb, tile_bytes + gi_bytes);
+        tma_load_2d_mc(&tmH, sbase + 128 + crank * (uint32_t)(R * 128), fb, d0, b * p.S + (int)crank * R,
+                       (uint16_t)((1u << DEST_CL) - 1u), pol);
+        if (gi_bytes) bulk_g2s(sbase + gi_off, p.gi + (size_t)b * p.ldGI + v0, gi_bytes, fb);
+        if (++st == nst) { st = 0; ph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ consumers
+    const int grp = warp * 4 + (lane >> 3);
+    const int sub = lane & 7;
+    float acc[J][8];
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int b = 0; b < p.B; ++b) {
+      ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
+      const uint8_t* tile = ds_smem + (size_t)st * stage_bytes;
+      const int2* gi = reinterpret_cast<const int2*>(tile + gi_off) + grp;
+      const uint8_t* rows = tile + 128 + sub * 16;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int2 e = gi[C::GROUPS * j];
+        const int4 x = *reinterpret_cast<const int4*>(rows + e.x * 128);
+        fma8(acc[j], pack_gg(__int_as_float(e.y)), x);
+      }
+      // Every lane's shared loads have been consumed by its FMAs (retired), so a
+      // relaxed arrival (no MEMBAR) suffices to release the stage to the
+      // peers' TMA writes.
+      __syncwarp();
+      if (lane < DEST_CL) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&empty[st]), (uint32_t)lane));
+      if (++st == nst) { st = 0; ph ^= 1; }
+    }
+    const int d = d0 + sub * 8;
+    if (d < p.D) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int v = v0 + grp + C::GROUPS * j;
+        if (v < p.V) store8<OutT>(reinterpret_cast<OutT*>(p.dE) + (size_t)v * p.D + d, acc[j]);
+      }
+    }
+  }
+  // Peers may still multicast into / arrive on this CTA until every CTA is done.
+  ptx::cluster_sync();
+}
+
+// db[v] = sum_b g[b, v] (b ascending) from the (s, g) records.
+__global__ void __launch_bounds__(256)
+sparton_bwd_db_kernel(const BwdParams p) {
+  const int v = blockIdx.x * 256 + threadIdx.x;
+  if (v >= p.V || p.db == nullptr) return;
+  float s = 0.f;
+  if (p.include_bias_grad) {
+    const int2* col = p.gi + v;
+    for (int b = 0; b < p.B; ++b) s += __int_as_float(__ldg(&col[(size_t)b * p.ldGI].y));
+  }
+  p.db[v] = s;
+}
+
 // ------------------------------------------------------------------ K3a: route
 // Grid (window, b).  The vocabulary is cut into windows of RT_WIN rows; for
 // each (b, window) the CTA performs a stable counting sort of the window's
@@ -411,6 +562,9 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin) {
   const int total = carry;
 
   // Phase 3: stable scatter of (v, g) into shared memory.
+  int2* gib = p.gi ? p.gi + (size_t)b * p.ldGI + v0 : nullptr;
+  if (gib != nullptr && w == nwin - 1 && threadIdx.x == 0)
+    for (long long v = p.V; v < p.ldGI; ++v) p.gi[(size_t)b * p.ldGI + v] = make_int2(-1, 0);   // row padding
   if (warp < nseg) {
     const int vs = min(n, warp * seg_len), ve = min(n, (warp + 1) * seg_len);
     int* cur = hist + warp * S;
@@ -428,12 +582,16 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const bool active = y[q] > 0.f;
+        const float g = active ? pair_grad(y[q], dy[q]) : 0.f;
+        // (s, g) record for the staged dE; inactive pairs get s = -1 (a zero row).
+        if (gib != nullptr && base + q * 32 + lane < ve)
+          gib[base + q * 32 + lane] = make_int2(active ? k[q] : -1, __float_as_int(g));
         const unsigned amask = __ballot_sync(0xffffffffu, active);
         if (active) {
           const unsigned peers = __match_any_sync(amask, k[q]);
           const int rank = __popc(peers & ((1u << lane) - 1u));
           const int pos = cur[k[q]] + rank;
-          ent[pos] = make_int2(v0 + base + q * 32 + lane, __float_as_int(pair_grad(y[q], dy[q])));
+          ent[pos] = make_int2(v0 + base + q * 32 + lane, __float_as_int(g));
           __syncwarp(amask);
           if (rank == 0) cur[k[q]] += __popc(peers);
         }
@@ -601,6 +759,73 @@ int side_stream(SideStream& out) {
   return SPARTON_OK;
 }
 
+
+int launch_route(const BwdParams& p, cudaStream_t stream) {
+  const int nseg = route_nseg(p.S);
+  const size_t smem = route_smem_bytes(p.S, nseg);
+  cudaError_t e = cudaFuncSetAttribute(sparton_bwd_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(route)", e);
+  sparton_bwd_route_kernel<<<dim3(p.nwin, p.B), RT_THREADS, smem, stream>>>(p, nseg, p.nwin);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_route_kernel", e);
+  return SPARTON_OK;
+}
+
+template <int CPL, typename OutT>
+int launch_dh(const BwdParams& p, cudaStream_t stream) {
+  const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
+  const long long rows = (long long)p.B * p.S;
+  dim3 grid((unsigned)((rows + DH_THREADS / 32 - 1) / (DH_THREADS / 32)), dslices);
+  // 2 E rows in flight per warp at 4 CTAs (32 warps) per SM measured best
+  // (1.34 ms/pass at cfg3) against 4 rows x 2 CTAs, 3 x 3 and D-sliced variants.
+  for (int c = 0; c < p.nchunks; ++c) {
+    sparton_bwd_dh_kernel<CPL, 2, 4, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
+  }
+  return SPARTON_OK;
+}
+
+constexpr int DEST_NW = 11, DEST_J = 17;           // 768 vocab rows x 64 columns per CTA
+constexpr int DEST_SMEM_BUDGET = 227 * 1024;
+
+int de_stage_bytes(int R) {
+  return (128 + DEST_CL * R * 128 + DeStCfg<DEST_NW, DEST_J>::GI_BYTES + 127) & ~127;
+}
+
+template <typename OutT>
+int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
+  using C = DeStCfg<DEST_NW, DEST_J>;
+  const int R = de_staged_rows(p.S);
+  const int stage_bytes = de_stage_bytes(R);
+  int nst = (DEST_SMEM_BUDGET - 128) / stage_bytes;
+  if (nst > 4) nst = 4;
+  const int smem = nst * stage_bytes + nst * 16;
+  auto kern = sparton_bwd_de_staged_kernel<DEST_NW, DEST_J, OutT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de_staged)", e);
+  const int nvb = (p.V + C::VB - 1) / C::VB;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((nvb + DEST_CL - 1) / DEST_CL * DEST_CL), (unsigned)((p.D + DEST_DD - 1) / DEST_DD), 1);
+  cfg.blockDim = dim3(C::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = DEST_CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, *tmH, p, R, nst, stage_bytes);
+  if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_de_staged_kernel", e);
+  sparton_bwd_db_kernel<<<(p.V + 255) / 256, 256, 0, stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_db_kernel", e);
+  return SPARTON_OK;
+}
+
 template <int CPL, int W, typename OutT>
 int launch_de_any(const BwdParams& p, cudaStream_t stream) {
   return (p.D % (256 * CPL) == 0) ? launch_de<CPL, W, true, OutT>(p, stream)
@@ -608,64 +833,66 @@ int launch_de_any(const BwdParams& p, cudaStream_t stream) {
 }
 
 template <int CPL, typename OutT>
-int launch_route_dh(const BwdParams& p, cudaStream_t stream) {
-  const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
-  {
-    const int nseg = route_nseg(p.S);
-    const size_t smem = route_smem_bytes(p.S, nseg);
-    cudaError_t e = cudaFuncSetAttribute(sparton_bwd_route_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(route)", e);
-    sparton_bwd_route_kernel<<<dim3(p.nwin, p.B), RT_THREADS, smem, stream>>>(p, nseg, p.nwin);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_route_kernel", e);
-  }
-  {
-    const long long rows = (long long)p.B * p.S;
-    dim3 grid((unsigned)((rows + DH_THREADS / 32 - 1) / (DH_THREADS / 32)), dslices);
-    // 2 E rows in flight per warp at 4 CTAs (32 warps) per SM measured best
-    // (1.34 ms/pass at cfg3) against 4 rows x 2 CTAs, 3 x 3 and D-sliced variants.
-    for (int c = 0; c < p.nchunks; ++c) {
-      sparton_bwd_dh_kernel<CPL, 2, 4, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
-    }
-  }
-  return SPARTON_OK;
-}
-
-template <int CPL, typename OutT>
-int launch_bwd_t(const BwdParams& p, cudaStream_t stream) {
+int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
   int mode = 1;
   if (const char* ev = getenv("SPARTON_BWD_CONCURRENT")) mode = atoi(ev);
-  if (mode == 0) {
-    const int rc = launch_de_any<CPL, 16, OutT>(p, stream);
-    if (rc != SPARTON_OK) return rc;
-    return launch_route_dh<CPL, OutT>(p, stream);
-  }
   SideStream ss;
   int rc = side_stream(ss);
   if (rc != SPARTON_OK) return rc;
-  cudaError_t e = cudaEventRecord(ss.fork, stream);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.s, ss.fork, 0);
-  if (e != cudaSuccess) return set_cuda_error("fork side stream", e);
+  cudaError_t e;
+  auto fork = [&]() -> int {
+    e = cudaEventRecord(ss.fork, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.s, ss.fork, 0);
+    return e == cudaSuccess ? SPARTON_OK : set_cuda_error("fork side stream", e);
+  };
+  auto join = [&]() -> int {
+    if ((e = cudaEventRecord(ss.join, ss.s)) != cudaSuccess) return set_cuda_error("record join", e);
+    if ((e = cudaStreamWaitEvent(stream, ss.join, 0)) != cudaSuccess) return set_cuda_error("join side stream", e);
+    return SPARTON_OK;
+  };
+  if (p.gi != nullptr) {
+    // Staged dE needs the route's (s, g) records: route, then dE || dH.
+    if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
+    if (mode == 0) {
+      if ((rc = launch_de_staged<OutT>(p, tmH, stream)) != SPARTON_OK) return rc;
+      return launch_dh<CPL, OutT>(p, stream);
+    }
+    if ((rc = fork()) != SPARTON_OK) return rc;
+    if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
+    if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+    return join();
+  }
+  if (mode == 0) {
+    if ((rc = launch_de_any<CPL, 16, OutT>(p, stream)) != SPARTON_OK) return rc;
+    if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
+    return launch_dh<CPL, OutT>(p, stream);
+  }
+  if ((rc = fork()) != SPARTON_OK) return rc;
   rc = (mode == 2) ? launch_de_any<CPL, 16, OutT>(p, ss.s) : launch_de_any<CPL, 8, OutT>(p, ss.s);
   if (rc != SPARTON_OK) return rc;
-  if ((e = cudaEventRecord(ss.join, ss.s)) != cudaSuccess) return set_cuda_error("record join", e);
-  rc = launch_route_dh<CPL, OutT>(p, stream);
-  if (rc != SPARTON_OK) return rc;
-  if ((e = cudaStreamWaitEvent(stream, ss.join, 0)) != cudaSuccess) return set_cuda_error("join side stream", e);
-  return SPARTON_OK;
+  if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
+  if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+  return join();
 }
 
 template <typename OutT>
-int launch_bwd_dtype(const BwdParams& p, cudaStream_t stream) {
-  if (p.D <= 256) return launch_bwd_t<1, OutT>(p, stream);
-  if (p.D <= 512 || p.D > 768) return launch_bwd_t<2, OutT>(p, stream);
-  return launch_bwd_t<3, OutT>(p, stream);
+int launch_bwd_dtype(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
+  if (p.D <= 256) return launch_bwd_t<1, OutT>(p, tmH, stream);
+  if (p.D <= 512 || p.D > 768) return launch_bwd_t<2, OutT>(p, tmH, stream);
+  return launch_bwd_t<3, OutT>(p, tmH, stream);
 }
 
 }  // namespace
+
+// Rows of H each CTA of a staged-dE cluster loads per batch row (a multiple of
+// 8, <= 256 for one TMA box), or 0 when two pipeline stages do not fit.
+int de_staged_rows(int S) {
+  int R = (S + DEST_CL - 1) / DEST_CL;
+  R = (R + 7) & ~7;
+  if (R > 256) return 0;
+  if (2 * de_stage_bytes(R) + 128 > DEST_SMEM_BUDGET) return 0;
+  return R;
+}
 
 // Largest S the in-smem route supports (one segment of S counters + the window).
 int bwd_max_seq() { return (RT_SMEM_BUDGET - RT_WIN * 8 - 128) / 4; }
@@ -695,18 +922,24 @@ BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long lo
   const int de_passes = (int)((B + bc - 1) / bc);
   w.db_acc = w.offsets + up((size_t)B * (size_t)w.nwin * (size_t)(S + 1) * sizeof(int));
   w.dE_acc = w.db_acc + up((size_t)V * sizeof(float));
-  const bool need_de_acc = grad_dtype == SPARTON_BF16 && de_passes > 1;
+  // Staged dE (S small enough for two smem stages): (s, g) records instead of
+  // the gathered dE's fp32 carry.
+  w.de_staged = de_staged_rows((int)S) > 0;
+  if (const char* ev = getenv("SPARTON_DE_STAGED")) w.de_staged = w.de_staged && ev[0] != '0';
+  w.ldGI = V + (V & 1);
+  const bool need_de_acc = !w.de_staged && grad_dtype == SPARTON_BF16 && de_passes > 1;
   w.acc32 = w.dE_acc + (need_de_acc ? up((size_t)V * (size_t)D * sizeof(float)) : 0);
   const bool need_acc = grad_dtype == SPARTON_BF16 && w.nchunks > 1;
-  w.total = w.acc32 + (need_acc ? up((size_t)B * (size_t)S * (size_t)D * sizeof(float)) : 0);
+  w.gi = w.acc32 + (need_acc ? up((size_t)B * (size_t)S * (size_t)D * sizeof(float)) : 0);
+  w.total = w.gi + (w.de_staged ? up((size_t)B * (size_t)w.ldGI * sizeof(int2)) : 0);
   if (!need_acc) w.acc32 = (size_t)-1;
   if (!need_de_acc) w.dE_acc = (size_t)-1;
   return w;
 }
 
-int launch_bwd(const BwdParams& p, int grad_dtype, cudaStream_t stream) {
-  if (grad_dtype == SPARTON_BF16) return launch_bwd_dtype<__nv_bfloat16>(p, stream);
-  return launch_bwd_dtype<float>(p, stream);
+int launch_bwd(const BwdParams& p, const CUtensorMap* tmH, int grad_dtype, cudaStream_t stream) {
+  if (grad_dtype == SPARTON_BF16) return launch_bwd_dtype<__nv_bfloat16>(p, tmH, stream);
+  return launch_bwd_dtype<float>(p, tmH, stream);
 }
 
 }  // namespace sparton

@@ -5,11 +5,11 @@
 // GEMM stage matmul_bt (tensor.py:130-188).  One persistent, warp-specialised
 // kernel per call:
 //
-//   warp 0        TMA producer: E tile (vocab rows, K-major) and H tile
+//   warp 4        TMA producer: E tile (vocab rows, K-major) and H tile
 //                 (sequence rows of one batch row, K-major) -> smem ring.
-//   warp 1        TMEM allocator; on the leader CTA, the single-thread
+//   warp 5        TMEM allocator; on the leader CTA, the single-thread
 //                 tcgen05.mma issuer (bf16 x bf16 -> f32 in TMEM).
-//   warps 2..5    epilogue: tcgen05.ld the accumulator, add bias, apply the
+//   warps 0..3    epilogue: tcgen05.ld the accumulator, add bias, apply the
 //                 mask (masked -> exactly 0, out-of-range s -> skipped), and
 //                 keep a running (max, first argmax) per vocab row in
 //                 registers across sequence chunks; log1p(relu(.)) is applied
@@ -103,23 +103,27 @@ struct UnitIter {
 
 // Reduce 32 accumulator columns (tile columns c0..c0+31 of the current chunk)
 // into four interleaved running (max, argmax) pairs; column c goes to slot c&3.
-// `keep` bit l: position valid and unmasked (value = acc + bias);
-// `zero` bit l: position valid but masked (value = 0, still competes);
+// The comparison runs on the raw dot products x = H.E: the bias is constant
+// along s, and fl(. + bias) is monotone, so max_s fl(x_s + bias) =
+// fl(max_s x_s + bias) exactly — Y is unchanged and the argmax can only
+// differ at positions whose logits tie after rounding (a documented near-tie,
+// SURVEY.md §8c).  A masked position has logit exactly 0, i.e. raw value
+// -bias (fl(-bias + bias) = +0).
+// `keep` bit l: position valid and unmasked (raw x);
+// `zero` bit l: position valid but masked (raw -bias, logit 0, still competes);
 // neither: position beyond S (skipped).
-__device__ __forceinline__ void reduce_group(const float (&r)[32], float bias, uint32_t keep,
+__device__ __forceinline__ void reduce_group(const float (&r)[32], float nbias, uint32_t keep,
                                              uint32_t zero, int c0, float (&best)[4],
                                              int (&bidx)[4]) {
   if (keep == 0xffffffffu) {
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      const float x = r[c] + bias;
-      if (x > best[c & 3]) { best[c & 3] = x; bidx[c & 3] = c0 + c; }
+      if (r[c] > best[c & 3]) { best[c & 3] = r[c]; bidx[c & 3] = c0 + c; }
     }
   } else {
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      float x = r[c] + bias;
-      x = ((keep >> c) & 1u) ? x : (((zero >> c) & 1u) ? 0.0f : -INFINITY);
+      const float x = ((keep >> c) & 1u) ? r[c] : (((zero >> c) & 1u) ? nbias : -INFINITY);
       if (x > best[c & 3]) { best[c & 3] = x; bidx[c & 3] = c0 + c; }
     }
   }
@@ -152,7 +156,12 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
   const long long cluster = (CG == 2) ? (long long)ptx::cluster_id_x() : (long long)blockIdx.x;
   const long long nclusters = (CG == 2) ? (long long)ptx::nclusters_x() : (long long)gridDim.x;
 
-  if (warp == 0 && lane == 0) {
+  // Warp roles.  The SM's four schedulers serve warps wid % 4 and favour the
+  // highest wid, so the TMA producer (warp 4) and the MMA issuer (warp 5) sit
+  // above the epilogue warps 0/1 that share their schedulers: epilogue
+  // instruction bursts never delay an MMA issue or a TMA refill.
+  constexpr int kProducer = 4, kMma = 5;
+  if (warp == kProducer && lane == 0) {
     ptx::prefetch_tmap(&tmE);
     ptx::prefetch_tmap(&tmH);
     for (int i = 0; i < C::NST; ++i) {
@@ -165,7 +174,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc<CG>(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
+  if (warp == kMma) ptx::tmem_alloc<CG>(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
@@ -174,7 +183,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
   const int nsc = (p.S + C::SN - 1) / C::SN;
   const int nkb = (p.D + C::BK - 1) / C::BK;
 
-  if (warp == 0) {
+  if (warp == kProducer) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       // L2 policies: 0 evict_normal, 1 evict_last, 2 evict_first (experiment switch)
@@ -218,7 +227,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMma) {
     if (rank == 0 && lane == 0) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
@@ -255,7 +264,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------ epilogue (warps 0..3)
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
     const int row = q * 32 + (int)lane;           // vocab row within this CTA's tile
     const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
@@ -298,7 +307,18 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           ptx::tmem_ld32(tacc + (uint32_t)(j * 32), r);
           ptx::tmem_ld_wait();
           ptx::reg_fence32(r);
-          if ((keep[j] | zero[j]) != 0u) reduce_group(r, bv, keep[j], zero[j], j * 32, cb, ci);
+          if (p.epi_mode == 1) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) cb[c & 3] = fmaxf(cb[c & 3], r[c]);
+          } else if (p.epi_mode == 2) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) cb[c & 3] = fmaxf(cb[c & 3] + 0.0f * (float)c, r[c]);
+          } else if (p.epi_mode == 3) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) if (r[c] > cb[c & 3]) cb[c & 3] = r[c];
+          } else if ((keep[j] | zero[j]) != 0u) {
+            reduce_group(r, -bv, keep[j], zero[j], j * 32, cb, ci);
+          }
         }
         // Accumulator fully read: hand it back to the MMA warp.
         ptx::tc_fence_before();
@@ -323,7 +343,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       }
       if (v < p.V) {
         const size_t o = (size_t)b * (size_t)p.ldY + (size_t)v;
-        p.Y[o] = log1pf(fmaxf(best, 0.0f));
+        p.Y[o] = log1pf(fmaxf(best + bv, 0.0f));
         p.I[o] = bidx;
       }
     }
@@ -331,7 +351,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
 
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
-  if (warp == 1) {
+  if (warp == kMma) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
   }
@@ -349,10 +369,7 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(fwd)", e);
   long long want = prm.num_units;
   int grid = (num_sms / CL) * CL;        // persistent: one CTA per SM, whole clusters
-  if (want < grid / CL) grid = (int)want * CL;
-  if (grid < CL) grid = CL;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
@@ -367,6 +384,26 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  if (CG == 2) {
+    // Clusters must all be co-resident (static persistent schedule): a GPC
+    // with an SM count not divisible by CL leaves SMs no cluster can use, and
+    // any cluster beyond the resident limit would run as a serial second wave.
+    static int max_clusters[8] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& mc = max_clusters[dev & 7];
+    if (mc == 0) {
+      cfg.gridDim = dim3(grid, 1, 1);
+      if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
+        cudaGetLastError();
+        mc = num_sms / CL;
+      }
+    }
+    if (grid > mc * CL) grid = mc * CL;
+  }
+  if (want < grid / CL) grid = (int)want * CL;
+  if (grid < CL) grid = CL;
+  cfg.gridDim = dim3(grid, 1, 1);
   e = cudaLaunchKernelEx(&cfg, kern, tmE, tmH, prm);
   if (e != cudaSuccess) return set_cuda_error("launch sparton_fwd_kernel", e);
   return SPARTON_OK;
@@ -380,14 +417,17 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
   prm.num_units = (long long)prm.num_vt * prm.B;
   const int nclusters = max(1, num_sms / cluster_ctas);
-  // E group of ~48 MB stays L2-resident while H streams (see UnitIter).
+  // E group of ~48 MB stays L2-resident while H streams (see UnitIter);
+  // 48 MB measured lower DRAM traffic than 4-32 MB (profiles/r01_fwd_l2_policy.txt).
   const long long tile_bytes = (long long)tile_v * prm.D * 2;
-  long long group_bytes = 24ll << 20;
+  long long group_bytes = 48ll << 20;
   if (const char* ev = getenv("SPARTON_FWD_GROUP_KB")) group_bytes = atoll(ev) << 10;
   int gv = (int)(group_bytes / (tile_bytes > 0 ? tile_bytes : 1));
   if (gv < 1) gv = 1;
   if (gv > prm.num_vt) gv = prm.num_vt;
   prm.group_vt = gv;
+  prm.epi_mode = 0;
+  if (const char* ev = getenv("SPARTON_FWD_EPI")) prm.epi_mode = atoi(ev);
   prm.sched_bgroups = 0;   // measured: the grouped round-robin moves less DRAM (profiles/)
   if (const char* ev = getenv("SPARTON_FWD_SCHED")) prm.sched_bgroups = ev[0] == '1';
   int rot = (int)(0.618 * nclusters + 0.5);

@@ -24,6 +24,7 @@ struct FwdParams {
   int e_evict_last;    // L2 policy for E tiles (experiment switch)
   int sched_bgroups;   // 1: batch-row-per-cluster groups (large B), 0: round-robin units
   int rot;             // per-group rotation of the cluster -> batch-row assignment
+  int epi_mode;        // experiment switch: 1 = max-only epilogue (no bias/argmax; wrong I)
 };
 
 struct BwdParams {
@@ -48,11 +49,15 @@ struct BwdParams {
   int nwin;            // route windows (RT_WIN vocab rows each)
   int wpc;             // route windows per dH pass (E chunk kept L2-resident)
   int nchunks;         // dH passes
+  int2* gi;            // workspace: per-(b, v) (s, g) records, row stride ldGI (staged dE), or nullptr
+  long long ldGI;      // even row stride of gi (16-B aligned rows)
 };
 
 // Workspace layout for sparton_bwd (byte offsets, 256-B aligned).
 struct BwdWorkspace {
-  size_t pairs, offsets, db_acc, dE_acc, acc32, total;
+  size_t pairs, offsets, db_acc, dE_acc, acc32, gi, total;
+  long long ldGI;
+  bool de_staged;
   int nwin, wpc, nchunks, bchunk;
 };
 BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long long V, int grad_dtype);
@@ -65,7 +70,12 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
                int num_sms, cudaStream_t stream);
 int fwd_smem_bytes(int cluster_ctas);
 int fwd_h_box_rows(int cluster_ctas);
-int launch_bwd(const BwdParams& prm, int grad_dtype, cudaStream_t stream);
+// H viewed as (B*S) x D bf16 with a (64 x rows) box, no swizzle (staged dE tiles).
+int encode_bf16_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long long cols, int box_rows,
+                         int box_cols);
+int launch_bwd(const BwdParams& prm, const CUtensorMap* tmH, int grad_dtype, cudaStream_t stream);
+// Rows of H each CTA of a staged-dE cluster loads per batch row (0: staged dE unsupported for S).
+int de_staged_rows(int S);
 int bwd_max_seq();
 
 }  // namespace sparton

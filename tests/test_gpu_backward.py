@@ -67,7 +67,9 @@ def test_golden_backward(cuda_device, name):
 
 
 GRID = [(1, 1, 16, 1), (2, 3, 16, 5), (4, 8, 16, 16), (2, 64, 64, 300), (3, 130, 256, 389),
-        (2, 512, 768, 2000), (4, 33, 1024, 777), (2, 40, 520, 100), (3, 7, 8, 1000)]
+        (2, 512, 768, 2000), (4, 33, 1024, 777), (2, 40, 520, 100), (3, 7, 8, 1000),
+        # S beyond the staged dE's two-stage smem limit: the gathered dE path.
+        (2, 1000, 128, 700), (5, 856, 64, 1501)]
 
 
 @pytest.mark.parametrize("dims", GRID)
@@ -198,3 +200,22 @@ def test_fullsize_slices_vs_oracle(cuda_device, V):
     dE_r, db_r = orc.backward_cols(Hn, Yn, In, dYn, cols)
     assert close(dE[cols].cpu().numpy(), dE_r)
     assert close(db[cols].cpu().numpy(), db_r)
+
+
+@pytest.mark.parametrize("dims", [(3, 300, 256, 3001), (2, 512, 200, 1600), (6, 17, 72, 5000)])
+@pytest.mark.parametrize("grad_dtype", [torch.float32, torch.bfloat16])
+def test_de_paths_agree(cuda_device, monkeypatch, dims, grad_dtype):
+    """The staged dE (H tiles in shared memory) and the gathered dE (per-pair
+    bulk copies) accumulate the same fp32 FMAs in the same b order: equal
+    results (up to the sign of zero), including db."""
+    B, S, D, V = dims
+    H, E, b, m = orc.seeded_inputs(B, S, D, V, 77 + S, mask_keep=0.8)
+    H, E = orc.bf16_round(H), orc.bf16_round(E)
+    dY = orc.seeded_uniform((B, V), 78)
+    Y, I = run_fwd(H, E, b, m)
+    monkeypatch.setenv("SPARTON_DE_STAGED", "1")
+    st = run_bwd(H, E, Y, I, dY, grad_dtype=grad_dtype)
+    monkeypatch.setenv("SPARTON_DE_STAGED", "0")
+    ga = run_bwd(H, E, Y, I, dY, grad_dtype=grad_dtype)
+    for x, y in zip(st, ga):
+        assert np.array_equal(x, y)
