@@ -88,10 +88,11 @@ __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_bar
                :: "r"(cluster_bar) : "memory");
 }
 
-// Blocking wait on phase parity (try_wait suspends in hardware until the phase
-// flips or a system time limit passes).  Bounded: after 2^26 polls (seconds)
-// the kernel traps instead of hanging the device, so a protocol bug surfaces
-// as a CUDA error rather than a wedged GPU.
+// Blocking wait on phase parity.  try_wait suspends the thread in hardware
+// until the phase flips or the suspend-time hint (ns) expires, so a long hint
+// keeps waiting warps off the issue slots instead of spinning.  Bounded:
+// after 2^20 polls (>= 20 s) the kernel traps instead of hanging the device,
+// so a protocol bug surfaces as a CUDA error rather than a wedged GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   uint32_t polls = 0;
@@ -99,13 +100,27 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, p;\n"
         "}\n"
-        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        : "=r"(done) : "r"(bar), "r"(parity), "n"(20000) : "memory");
     if (done) return;
-    if (++polls == (1u << 26)) __trap();
+    if (++polls == (1u << 20)) __trap();
   }
+}
+
+// One elected lane of a converged warp (elect.sync): warp-uniform control flow
+// around single-thread tcgen05 / TMA issue keeps loop state in uniform registers.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "elect.sync _|P1, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "+r"(pred));
+  return pred != 0;
 }
 
 // ---------------------------------------------------------------- TMA

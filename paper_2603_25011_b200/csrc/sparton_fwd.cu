@@ -65,22 +65,24 @@ struct FwdCfg {
 // Default / small B: round-robin over units ordered (vocab group, b, tile).
 struct UnitIter {
   int g = 0, j = 0, k = 0;
-  long long u = 0;
+  unsigned u = 0;
   int c, nc;
-  __device__ UnitIter(int cluster, int nclusters) : c(cluster), nc(nclusters) { u = cluster; }
+  __device__ UnitIter(int cluster, int nclusters) : c(cluster), nc(nclusters) { u = (unsigned)cluster; }
   __device__ __forceinline__ bool next(const FwdParams& p, int& b, int& vt) {
     if (!p.sched_bgroups) {
       // Round-robin over units ordered (vocab group, b, tile): consecutive
       // clusters share H[b] and the group's E tiles stay L2-resident.
-      if (u >= p.num_units) return false;
-      const long long per_group = (long long)p.group_vt * p.B;
-      const long long gg = u / per_group;
-      const long long r = u - gg * per_group;
+      // (num_units < 2^31 is checked on the host: 32-bit index math.)
+      if (u >= (unsigned)p.num_units) return false;
+      const unsigned per_group = (unsigned)p.group_vt * (unsigned)p.B;
+      const unsigned gg = u / per_group;
+      const unsigned r = u - gg * per_group;
       const int gv0 = (int)gg * p.group_vt;
-      const int gsz = min(p.group_vt, p.num_vt - gv0);
-      b = (int)(r / gsz);
-      vt = gv0 + (int)(r % gsz);
-      u += nc;
+      const unsigned gsz = (unsigned)min(p.group_vt, p.num_vt - gv0);
+      const unsigned bb = r / gsz;
+      b = (int)bb;
+      vt = gv0 + (int)(r - bb * gsz);
+      u += (unsigned)nc;
       return true;
     }
     while (true) {
@@ -184,24 +186,26 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
   const int nkb = (p.D + C::BK - 1) / C::BK;
 
   if (warp == kProducer) {
-    if (lane == 0) {
-      // ------------------------------------------------ TMA producer
-      // L2 policies: 0 evict_normal, 1 evict_last, 2 evict_first (experiment switch)
-      auto pol = [](int k) {
-        return k == 1 ? ptx::policy_evict_last() : (k == 2 ? ptx::policy_evict_first() : ptx::policy_evict_normal());
-      };
-      const uint64_t pol_e = pol(p.e_evict_last & 3);
-      const uint64_t pol_h = pol((p.e_evict_last >> 2) & 3);
-      int st = 0;
-      uint32_t ph = 0;
-      UnitIter it((int)cluster, (int)nclusters);
-      int b, vt;
-      while (it.next(p, b, vt)) {
-        const int vrow = vt * C::TILE_V + (int)pair * (C::BM * CG) + (int)rank * C::BM;
-        for (int sc = 0; sc < nsc; ++sc) {
-          const int hrow = b * p.S + sc * C::SN + (int)rank * C::BN_CTA + (int)pair * C::BN_LOAD;
-          for (int kb = 0; kb < nkb; ++kb) {
-            ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
+    // ------------------------------------------------ TMA producer
+    // The whole warp walks the schedule (warp-uniform state); one elected
+    // lane issues each stage's barrier arm and TMA loads.
+    // L2 policies: 0 evict_normal, 1 evict_last, 2 evict_first (experiment switch)
+    auto pol = [](int k) {
+      return k == 1 ? ptx::policy_evict_last() : (k == 2 ? ptx::policy_evict_first() : ptx::policy_evict_normal());
+    };
+    const uint64_t pol_e = pol(p.e_evict_last & 3);
+    const uint64_t pol_h = pol((p.e_evict_last >> 2) & 3);
+    int st = 0;
+    uint32_t ph = 0;
+    UnitIter it((int)cluster, (int)nclusters);
+    int b, vt;
+    while (it.next(p, b, vt)) {
+      const int vrow = vt * C::TILE_V + (int)pair * (C::BM * CG) + (int)rank * C::BM;
+      for (int sc = 0; sc < nsc; ++sc) {
+        const int hrow = b * p.S + sc * C::SN + (int)rank * C::BN_CTA + (int)pair * C::BN_LOAD;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
+          if (ptx::elect_one()) {
             const uint32_t sa = ptx::smem_u32(stage_base + st * C::STAGE_BYTES);
             const uint32_t sb = sa + C::A_BYTES;
             const uint32_t fb = ptx::smem_u32(&full[st]);
@@ -222,14 +226,16 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
                                         pol_h);
               }
             }
-            if (++st == C::NST) { st = 0; ph ^= 1; }
           }
+          __syncwarp();
+          if (++st == C::NST) { st = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == kMma) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
       // ------------------------------------------------ MMA issuer
+      // Warp-uniform loop; one elected lane issues the MMAs and commits.
       constexpr uint32_t idesc = ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
       int st = 0;
       uint32_t ph = 0;
@@ -245,19 +251,23 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           for (int kb = 0; kb < nkb; ++kb) {
             ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
             ptx::tc_fence_after();
-            const uint32_t sa = ptx::smem_u32(stage_base + st * C::STAGE_BYTES);
-            const uint64_t da = ptx::umma_desc_sw128(sa);
-            const uint64_t db = ptx::umma_desc_sw128(sa + C::A_BYTES);
+            if (ptx::elect_one()) {
+              const uint32_t sa = ptx::smem_u32(stage_base + st * C::STAGE_BYTES);
+              const uint64_t da = ptx::umma_desc_sw128(sa);
+              const uint64_t db = ptx::umma_desc_sw128(sa + C::A_BYTES);
 #pragma unroll
-            for (int k = 0; k < C::BK / 16; ++k) {
-              // +32 bytes along K inside the 128-B swizzle row = +2 in the >>4 address field.
-              ptx::umma_bf16<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+              for (int k = 0; k < C::BK / 16; ++k) {
+                // +32 bytes along K inside the 128-B swizzle row = +2 in the >>4 address field.
+                ptx::umma_bf16<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+              }
+              // The stage's H half was written by every pair's producer: release it cluster-wide.
+              ptx::umma_commit<CG>(ptx::smem_u32(&empty[st]), all_mask);
             }
-            // The stage's H half was written by every pair's producer: release it cluster-wide.
-            ptx::umma_commit<CG>(ptx::smem_u32(&empty[st]), all_mask);
+            __syncwarp();
             if (++st == C::NST) { st = 0; ph ^= 1; }
           }
-          ptx::umma_commit<CG>(ptx::smem_u32(&tfull[acc]), pair_mask);
+          if (ptx::elect_one()) ptx::umma_commit<CG>(ptx::smem_u32(&tfull[acc]), pair_mask);
+          __syncwarp();
           acc ^= 1;
           if (acc == 0) aph ^= 1;
         }
@@ -288,13 +298,23 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         const int s0 = sc * C::SN;
         // Mask words for the 8 column groups of this chunk (warp-uniform).
         uint32_t keep[8], zero[8];
+        if (s0 + C::SN <= p.S) {
+          // Full chunk: one base address, eight byte loads, eight ballots.
+          const uint8_t* mp = mrow + s0 + lane;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int s = s0 + j * 32 + (int)lane;
-          const bool valid = s < p.S;
-          const bool m = valid && (__ldg(mrow + (valid ? s : 0)) != 0);
-          keep[j] = __ballot_sync(0xffffffffu, m);
-          zero[j] = __ballot_sync(0xffffffffu, valid && !m);
+          for (int j = 0; j < 8; ++j) {
+            keep[j] = __ballot_sync(0xffffffffu, __ldg(mp + j * 32) != 0);
+            zero[j] = ~keep[j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int s = s0 + j * 32 + (int)lane;
+            const bool valid = s < p.S;
+            const bool m = valid && (__ldg(mrow + (valid ? s : 0)) != 0);
+            keep[j] = __ballot_sync(0xffffffffu, m);
+            zero[j] = __ballot_sync(0xffffffffu, valid && !m);
+          }
         }
         ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), aph);
         ptx::tc_fence_after();
@@ -416,6 +436,8 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   const int tile_v = 128 * cluster_ctas;
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
   prm.num_units = (long long)prm.num_vt * prm.B;
+  if (prm.num_units >= (1ll << 31) - 4096)
+    return set_error(SPARTON_EINVAL, "B * ceil(V / vocab_tile) exceeds the forward scheduler's 31-bit unit index");
   const int nclusters = max(1, num_sms / cluster_ctas);
   // E group of ~48 MB stays L2-resident while H streams (see UnitIter);
   // 48 MB measured lower DRAM traffic than 4-32 MB (profiles/r01_fwd_l2_policy.txt).
