@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <mutex>
 
 #include "ptx.cuh"
@@ -55,7 +56,8 @@ __device__ __forceinline__ float pair_grad(float y, float dy) {
 // acc[0..7] += g * bf16x8(raw), as four packed fp32x2 FMAs (FFMA2: two
 // independent round-to-nearest fp32 FMAs, bit-identical to scalar fmaf).
 // bf16 -> fp32 is exact: the low half of each 32-bit word moves to the top
-// (shl 16), the high half is masked in place.
+// (byte permute), the high half is masked in place — both on the ALU pipe, so
+// the FMA pipe only carries the FFMA2s.
 __device__ __forceinline__ uint64_t pack_gg(float g) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(g));
@@ -67,7 +69,7 @@ __device__ __forceinline__ void fma8(float* acc, uint64_t gg, const int4& raw) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     asm("{\n.reg .b32 lo, hi;\n.reg .b64 x, a;\n"
-        "shl.b32 lo, %2, 16;\n"
+        "prmt.b32 lo, %2, 0, 0x1044;\n"
         "and.b32 hi, %2, 0xffff0000;\n"
         "mov.b64 x, {lo, hi};\n"
         "mov.b64 a, {%0, %1};\n"
@@ -614,13 +616,16 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin) {
 // each in ascending v, so the accumulation order is exactly the reference's
 // (v ascending, hidden_row / np.add.at).  Partial sums carry across launches in
 // fp32 (the output itself when it is fp32, else the workspace accumulator).
-template <int CPL, int DH_UNROLL, int MINB, typename OutT>
-__global__ void __launch_bounds__(DH_THREADS, MINB)
+template <int CPL, int DH_UNROLL, int MINB, bool FULL, typename OutT, int THREADS = DH_THREADS>
+__global__ void __launch_bounds__(THREADS, MINB)
 sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const long long rowid = (long long)blockIdx.x * (DH_THREADS / 32) + warp;   // b*S + s
-  if (rowid >= (long long)p.B * p.S) return;
+  const long long nrows = (long long)p.B * p.S;
+  // Grid-stride over rows (b*S + s): the grid may be smaller than the row count
+  // so dH can run persistently on part of the GPU next to the staged dE.
+  for (long long rowid = (long long)blockIdx.x * (THREADS / 32) + warp; rowid < nrows;
+       rowid += (long long)gridDim.x * (THREADS / 32)) {
   const int b = (int)(rowid / p.S);
   const int s = (int)(rowid - (long long)b * p.S);
   const int d0 = blockIdx.y * (256 * CPL);
@@ -631,7 +636,7 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
 
   bool dvalid[CPL];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) dvalid[c] = (d0 + c * 256 + lane * 8) < p.D;
+  for (int c = 0; c < CPL; ++c) dvalid[c] = FULL || (d0 + c * 256 + lane * 8) < p.D;
   float acc[CPL * 8];
   float* accg = p.acc32 ? p.acc32 : reinterpret_cast<float*>(p.dH);   // fp32 carry buffer
   if (first) {
@@ -706,6 +711,7 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
     for (int c = 0; c < CPL; ++c)
       if (dvalid[c]) store8<float>(dst + c * 256, &acc[c * 8]);
   }
+  }  // rows
 }
 
 int route_nseg(int S) {
@@ -776,33 +782,53 @@ template <int CPL, typename OutT>
 int launch_dh(const BwdParams& p, cudaStream_t stream) {
   const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
   const long long rows = (long long)p.B * p.S;
-  dim3 grid((unsigned)((rows + DH_THREADS / 32 - 1) / (DH_THREADS / 32)), dslices);
+  long long gx = (rows + DH_THREADS / 32 - 1) / (DH_THREADS / 32);
+  if (const char* ev = getenv("SPARTON_DH_CTAS")) {   // experiment switch: persistent grid size
+    const long long n = atoll(ev);
+    if (n > 0 && n < gx) gx = n;
+  }
+  dim3 grid((unsigned)gx, dslices);
   // 2 E rows in flight per warp at 4 CTAs (32 warps) per SM measured best
   // (1.34 ms/pass at cfg3) against 4 rows x 2 CTAs, 3 x 3 and D-sliced variants.
+  const bool full = p.D % (256 * CPL) == 0;
+  if (const char* ev = getenv("SPARTON_DH_FAT")) {   // experiment: n persistent 1024-thread CTAs (1 per SM)
+    const int n = atoi(ev);
+    if (n > 0 && full) {
+      for (int c = 0; c < p.nchunks; ++c) {
+        sparton_bwd_dh_kernel<CPL, 2, 1, true, OutT, 1024><<<dim3(n, dslices), 1024, 0, stream>>>(p, c);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
+      }
+      return SPARTON_OK;
+    }
+  }
   for (int c = 0; c < p.nchunks; ++c) {
-    sparton_bwd_dh_kernel<CPL, 2, 4, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
+    if (full) sparton_bwd_dh_kernel<CPL, 2, 4, true, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
+    else sparton_bwd_dh_kernel<CPL, 2, 4, false, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
   }
   return SPARTON_OK;
 }
 
-constexpr int DEST_NW = 11, DEST_J = 17;           // 768 vocab rows x 64 columns per CTA
 constexpr int DEST_SMEM_BUDGET = 227 * 1024;
 
-int de_stage_bytes(int R) {
-  return (128 + DEST_CL * R * 128 + DeStCfg<DEST_NW, DEST_J>::GI_BYTES + 127) & ~127;
+template <int NW, int J>
+int de_stage_bytes_t(int R) {
+  return (128 + DEST_CL * R * 128 + DeStCfg<NW, J>::GI_BYTES + 127) & ~127;
 }
+// Largest GI block of the configurations below (sizes the two-stage check).
+int de_stage_bytes(int R) { return de_stage_bytes_t<11, 17>(R); }
 
-template <typename OutT>
-int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
-  using C = DeStCfg<DEST_NW, DEST_J>;
+template <int NW, int J, typename OutT>
+int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
+  using C = DeStCfg<NW, J>;
   const int R = de_staged_rows(p.S);
-  const int stage_bytes = de_stage_bytes(R);
+  const int stage_bytes = de_stage_bytes_t<NW, J>(R);
   int nst = (DEST_SMEM_BUDGET - 128) / stage_bytes;
   if (nst > 4) nst = 4;
   const int smem = nst * stage_bytes + nst * 16;
-  auto kern = sparton_bwd_de_staged_kernel<DEST_NW, DEST_J, OutT>;
+  auto kern = sparton_bwd_de_staged_kernel<NW, J, OutT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de_staged)", e);
   const int nvb = (p.V + C::VB - 1) / C::VB;
@@ -824,6 +850,16 @@ int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t st
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_db_kernel", e);
   return SPARTON_OK;
+}
+
+// Register budget split between accumulators (reuse: VB vocab rows per staged
+// H tile) and loads in flight (latency hiding): 15 consumer warps x 12 rows
+// (128 regs) vs 11 x 17 (168 regs); SPARTON_DEST_CFG=1 selects the latter.
+template <typename OutT>
+int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
+  const char* ev = getenv("SPARTON_DEST_CFG");
+  if (ev && ev[0] == '1') return launch_de_staged_t<11, 17, OutT>(p, tmH, stream);
+  return launch_de_staged_t<15, 12, OutT>(p, tmH, stream);
 }
 
 template <int CPL, int W, typename OutT>
@@ -857,6 +893,35 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
       if ((rc = launch_de_staged<OutT>(p, tmH, stream)) != SPARTON_OK) return rc;
       return launch_dh<CPL, OutT>(p, stream);
     }
+    if (mode == 5) {   // dH first (persistent grid grabs its SMs), then dE on the side stream
+      static cudaEvent_t ev[5];
+      static bool init = false;
+      const bool dbg = getenv("SPARTON_BWD_EVENTS") != nullptr;
+      if (dbg && !init) { for (auto& x : ev) cudaEventCreate(&x); init = true; }
+      if (dbg) cudaEventRecord(ev[0], stream);
+      if ((rc = fork()) != SPARTON_OK) return rc;
+      if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+      if (dbg) { cudaEventRecord(ev[1], stream); cudaEventRecord(ev[2], ss.s); }
+      if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
+      if (dbg) cudaEventRecord(ev[3], ss.s);
+      rc = join();
+      if (dbg) {
+        cudaEventSynchronize(ev[3]);
+        cudaEventSynchronize(ev[1]);
+        float a, b, c;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[0], ev[2]);
+        cudaEventElapsedTime(&c, ev[0], ev[3]);
+        fprintf(stderr, "bwd events: dH end %.2f  dE start %.2f  dE end %.2f ms\n", a, b, c);
+      }
+      return rc;
+    }
+    if (mode == 6) {   // experiment: dH then dE, one stream
+      if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+      return launch_de_staged<OutT>(p, tmH, stream);
+    }
+    if (mode == 3) return launch_de_staged<OutT>(p, tmH, stream);   // experiment: dE only
+    if (mode == 4) return launch_dh<CPL, OutT>(p, stream);          // experiment: dH only
     if ((rc = fork()) != SPARTON_OK) return rc;
     if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
     if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
@@ -906,7 +971,9 @@ BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long lo
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   BwdWorkspace w{};
   w.nwin = (int)((V + RT_WIN - 1) / RT_WIN);
-  long long wpc = DH_CHUNK_BYTES / ((long long)RT_WIN * D * 2);
+  long long chunk_bytes = DH_CHUNK_BYTES;
+  if (const char* ev = getenv("SPARTON_DH_CHUNK_MB")) chunk_bytes = atoll(ev) << 20;   // experiment switch
+  long long wpc = chunk_bytes / ((long long)RT_WIN * D * 2);
   if (wpc < 1) wpc = 1;
   if (wpc > w.nwin) wpc = w.nwin;
   w.wpc = (int)wpc;
