@@ -50,6 +50,17 @@ def flops(c):
     return 2 * c["B"] * c["S"] * c["V"] * c["D"], 4 * c["B"] * c["V"] * c["D"]
 
 
+def launches_per_step(c, v_local):
+    """Kernels the library launches per step (fwd + bwd) on one rank:
+    K1 + route + staged dE + db column sum + one dH launch per L2-sized
+    vocabulary chunk (csrc/sparton_bwd.cu: RT_WIN = 8192 rows per route
+    window, DH_CHUNK_BYTES = 40 MB of E per chunk)."""
+    D = c["D"]
+    nwin = -(-v_local // 8192)
+    wpc = max(1, min(nwin, 32, (40 << 20) // (8192 * D * 2)))
+    return 1 + 1 + 1 + 1 + -(-nwin // wpc)
+
+
 def measured_peaks():
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -291,7 +302,7 @@ def run_gpu_arm(args, c, cname):
                      "frac_of_burst": achieved / peaks["bf16_tflops"],
                      "traffic": ncu_traffic(cname), "algorithmic_flops_per_launch": fwd_flops_rank,
                      "peak_source": peaks["source"] + " (sustained; burst in frac_of_burst)"},
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": launches_per_step(c, v1 - v0) * args.steps,
         "clocks": clocks,
     }
     if e2e is not None:
