@@ -15,6 +15,9 @@ import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libsparton_b200.so"
+# Development override (A/B timing of two builds); the product path uses the in-tree library.
+if os.environ.get("SPARTON_LIB"):
+    LIB_PATH = Path(os.environ["SPARTON_LIB"]).resolve()
 
 SPARTON_OK = 0
 SPARTON_EINVAL = 1

@@ -424,8 +424,9 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
     for (int b = 0; b < p.B; ++b) {
       ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
       const uint8_t* tile = ds_smem + (size_t)st * stage_bytes;
-      const int2* gi = reinterpret_cast<const int2*>(tile + gi_off) + grp;
       const uint8_t* rows = tile + 128 + sub * 16;
+      // Group grp owns vocab rows grp + GROUPS*j: one broadcast record load each.
+      const int2* gi = reinterpret_cast<const int2*>(tile + gi_off) + grp;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const int2 e = gi[C::GROUPS * j];
@@ -479,7 +480,7 @@ constexpr int RT_WIN = 8192;
 constexpr int RT_SMEM_BUDGET = 200 * 1024;
 
 __global__ void __launch_bounds__(RT_THREADS)
-sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin) {
+sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash) {
   extern __shared__ int4 rt_smem[];
   const int S = p.S;
   int2* ent = reinterpret_cast<int2*>(rt_smem);       // [RT_WIN] sorted (v, g)
@@ -500,22 +501,59 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin) {
   const int32_t* Ib = p.I + (size_t)b * p.ldY + v0;
   const float* dYb = p.dY + (size_t)b * p.ldDY + v0;
 
-  // Phase 1: per-segment histograms (4 x 32 loads in flight per warp).
+  // Phase 1: per-segment histograms.  When a warp's segment fits its register
+  // stash (every warp owns a segment: S <= 2125), Y/I/dY are read once here:
+  // g and the staged dE's (s, g) record are produced now and (s, g) kept in
+  // registers for the scatter, so phase 3 touches no global memory.
+  constexpr int RQ = RT_WIN / RT_THREADS;   // stashed elements per lane
+  const bool stash = allow_stash && seg_len <= 32 * RQ;
+  int rk[RQ];
+  float rg[RQ];
+  int2* gib = p.gi ? p.gi + (size_t)b * p.ldGI + v0 : nullptr;
+  if (gib != nullptr && w == nwin - 1 && threadIdx.x == 0)
+    for (long long v = p.V; v < p.ldGI; ++v) p.gi[(size_t)b * p.ldGI + v] = make_int2(-1, 0);   // row padding
   if (warp < nseg) {
     const int vs = min(n, warp * seg_len), ve = min(n, (warp + 1) * seg_len);
     int* h = hist + warp * S;
-    for (int base = vs; base < ve; base += 128) {
-      float y[4];
-      int k[4];
+    if (stash) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int v = base + q * 32 + lane;
-        y[q] = v < ve ? Yb[v] : 0.f;
-        k[q] = v < ve ? Ib[v] : 0;
+      for (int q0 = 0; q0 < RQ; q0 += 4) {
+        float y[4], dy[4];
+        int k[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = vs + (q0 + q) * 32 + lane;
+          const bool in = v < ve;
+          y[q] = in ? Yb[v] : 0.f;
+          k[q] = in ? Ib[v] : 0;
+          dy[q] = in ? dYb[v] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = vs + (q0 + q) * 32 + lane;
+          const bool active = y[q] > 0.f;
+          const float g = active ? pair_grad(y[q], dy[q]) : 0.f;
+          // (s, g) record for the staged dE; inactive pairs get s = -1 (a zero row).
+          if (gib != nullptr && v < ve) gib[v] = make_int2(active ? k[q] : -1, __float_as_int(g));
+          if (active) atomicAdd(&h[k[q]], 1);
+          rk[q0 + q] = active ? k[q] : -1;
+          rg[q0 + q] = g;
+        }
       }
+    } else {
+      for (int base = vs; base < ve; base += 128) {
+        float y[4];
+        int k[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (y[q] > 0.f) atomicAdd(&h[k[q]], 1);
+        for (int q = 0; q < 4; ++q) {
+          const int v = base + q * 32 + lane;
+          y[q] = v < ve ? Yb[v] : 0.f;
+          k[q] = v < ve ? Ib[v] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (y[q] > 0.f) atomicAdd(&h[k[q]], 1);
+      }
     }
   }
   __syncthreads();
@@ -563,41 +601,47 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin) {
   if (threadIdx.x == 0) off[S] = carry;
   const int total = carry;
 
-  // Phase 3: stable scatter of (v, g) into shared memory.
-  int2* gib = p.gi ? p.gi + (size_t)b * p.ldGI + v0 : nullptr;
-  if (gib != nullptr && w == nwin - 1 && threadIdx.x == 0)
-    for (long long v = p.V; v < p.ldGI; ++v) p.gi[(size_t)b * p.ldGI + v] = make_int2(-1, 0);   // row padding
+  // Phase 3: stable scatter of (v, g) into shared memory.  Equal keys inside a
+  // warp are ranked by lane order (match.any); the bucket cursor then advances.
   if (warp < nseg) {
     const int vs = min(n, warp * seg_len), ve = min(n, (warp + 1) * seg_len);
     int* cur = hist + warp * S;
-    for (int base = vs; base < ve; base += 128) {
-      float y[4], dy[4];
-      int k[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int v = base + q * 32 + lane;
-        const bool in = v < ve;
-        y[q] = in ? Yb[v] : 0.f;
-        k[q] = in ? Ib[v] : 0;
-        dy[q] = in ? dYb[v] : 0.f;
+    auto place = [&](int k, float g, int v) {
+      const bool active = k >= 0;
+      const unsigned amask = __ballot_sync(0xffffffffu, active);
+      if (active) {
+        const unsigned peers = __match_any_sync(amask, k);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        const int pos = cur[k] + rank;
+        ent[pos] = make_int2(v0 + v, __float_as_int(g));
+        __syncwarp(amask);
+        if (rank == 0) cur[k] += __popc(peers);
       }
+      __syncwarp();
+    };
+    if (stash) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool active = y[q] > 0.f;
-        const float g = active ? pair_grad(y[q], dy[q]) : 0.f;
-        // (s, g) record for the staged dE; inactive pairs get s = -1 (a zero row).
-        if (gib != nullptr && base + q * 32 + lane < ve)
-          gib[base + q * 32 + lane] = make_int2(active ? k[q] : -1, __float_as_int(g));
-        const unsigned amask = __ballot_sync(0xffffffffu, active);
-        if (active) {
-          const unsigned peers = __match_any_sync(amask, k[q]);
-          const int rank = __popc(peers & ((1u << lane) - 1u));
-          const int pos = cur[k[q]] + rank;
-          ent[pos] = make_int2(v0 + base + q * 32 + lane, __float_as_int(g));
-          __syncwarp(amask);
-          if (rank == 0) cur[k[q]] += __popc(peers);
+      for (int q = 0; q < RQ; ++q) place(rk[q], rg[q], vs + q * 32 + lane);
+    } else {
+      for (int base = vs; base < ve; base += 128) {
+        float y[4], dy[4];
+        int k[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = base + q * 32 + lane;
+          const bool in = v < ve;
+          y[q] = in ? Yb[v] : 0.f;
+          k[q] = in ? Ib[v] : 0;
+          dy[q] = in ? dYb[v] : 0.f;
         }
-        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = base + q * 32 + lane;
+          const bool active = y[q] > 0.f;
+          const float g = active ? pair_grad(y[q], dy[q]) : 0.f;
+          if (gib != nullptr && v < ve) gib[v] = make_int2(active ? k[q] : -1, __float_as_int(g));
+          place(active ? k[q] : -1, g, v);
+        }
       }
     }
   }
@@ -658,44 +702,67 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
     }
   }
 
-  for (int w = w0; w < w1; ++w) {
-    const int* off = p.offsets + ((size_t)b * p.nwin + w) * (p.S + 1);
-    const int k1 = off[s + 1];
-    const int2* lst = p.pairs + (size_t)b * p.V + (size_t)w * RT_WIN;
-    for (int k = off[s]; k < k1; k += 32) {
-      const int m = min(32, k1 - k);
-      int2 mine = make_int2(0, 0);
-      if (lane < m) mine = lst[k + lane];
-      int j = 0;
-      for (; j + DH_UNROLL <= m; j += DH_UNROLL) {
-        float gq[DH_UNROLL];
-        int4 xq[DH_UNROLL][CPL];
+  // The row's sub-lists of every window of this pass, read as one flattened
+  // list: lane t < nw fetches window w0+t's bounds (one round trip for all
+  // windows), a prefix sum over lanes gives each window's start in the
+  // flattened order, and each batch of 32 records is fetched in one load
+  // (window order, then ascending v: the reference's summation order).
+  const int nw = w1 - w0;                  // <= 32 (wpc is capped on the host)
+  int ks = 0, cnt = 0;
+  if (lane < nw) {
+    const int* off = p.offsets + ((size_t)b * p.nwin + w0 + lane) * (p.S + 1);
+    ks = off[s];
+    cnt = off[s + 1] - ks;
+  }
+  int incl = cnt;
 #pragma unroll
-        for (int q = 0; q < DH_UNROLL; ++q) {
-          const int vq = __shfl_sync(0xffffffffu, mine.x, j + q);
-          gq[q] = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j + q));
-          const __nv_bfloat16* r = p.E + (size_t)vq * p.D + d0 + lane * 8;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int excl = incl - cnt;             // flattened start of window lane (lane < nw)
+  const int2* lst0 = p.pairs + (size_t)b * p.V + (size_t)w0 * RT_WIN;
+  for (int base = 0; base < total; base += 32) {
+    const int m = min(32, total - base);
+    const int idx = base + lane;
+    int wsel = 0, e_sel = 0, k_sel = 0;
+    for (int t = 0; t < nw; ++t) {
+      const int et = __shfl_sync(0xffffffffu, excl, t);
+      const int kt = __shfl_sync(0xffffffffu, ks, t);
+      if (idx >= et) { wsel = t; e_sel = et; k_sel = kt; }
+    }
+    int2 mine = make_int2(0, 0);
+    if (lane < m) mine = lst0[(size_t)wsel * RT_WIN + k_sel + (idx - e_sel)];
+    int j = 0;
+    for (; j + DH_UNROLL <= m; j += DH_UNROLL) {
+      float gq[DH_UNROLL];
+      int4 xq[DH_UNROLL][CPL];
 #pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            xq[q][c] = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
-        }
+      for (int q = 0; q < DH_UNROLL; ++q) {
+        const int vq = __shfl_sync(0xffffffffu, mine.x, j + q);
+        gq[q] = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j + q));
+        const __nv_bfloat16* r = p.E + (size_t)vq * p.D + d0 + lane * 8;
 #pragma unroll
-        for (int q = 0; q < DH_UNROLL; ++q) {
-          const uint64_t gg = pack_gg(gq[q]);
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) fma8(&acc[c * 8], gg, xq[q][c]);
-        }
+        for (int c = 0; c < CPL; ++c)
+          xq[q][c] = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
       }
-      for (; j < m; ++j) {
-        const int va = __shfl_sync(0xffffffffu, mine.x, j);
-        const float ga = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j));
-        const __nv_bfloat16* r = p.E + (size_t)va * p.D + d0 + lane * 8;
-        const uint64_t gg = pack_gg(ga);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const int4 x = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
-          fma8(&acc[c * 8], gg, x);
-        }
+      for (int q = 0; q < DH_UNROLL; ++q) {
+        const uint64_t gg = pack_gg(gq[q]);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) fma8(&acc[c * 8], gg, xq[q][c]);
+      }
+    }
+    for (; j < m; ++j) {
+      const int va = __shfl_sync(0xffffffffu, mine.x, j);
+      const float ga = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j));
+      const __nv_bfloat16* r = p.E + (size_t)va * p.D + d0 + lane * 8;
+      const uint64_t gg = pack_gg(ga);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int4 x = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
+        fma8(&acc[c * 8], gg, x);
       }
     }
   }
@@ -772,7 +839,9 @@ int launch_route(const BwdParams& p, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(sparton_bwd_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(route)", e);
-  sparton_bwd_route_kernel<<<dim3(p.nwin, p.B), RT_THREADS, smem, stream>>>(p, nseg, p.nwin);
+  int allow_stash = 1;
+  if (const char* ev = getenv("SPARTON_ROUTE_STASH")) allow_stash = atoi(ev);   // experiment switch
+  sparton_bwd_route_kernel<<<dim3(p.nwin, p.B), RT_THREADS, smem, stream>>>(p, nseg, p.nwin, allow_stash);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_route_kernel", e);
   return SPARTON_OK;
@@ -817,8 +886,8 @@ template <int NW, int J>
 int de_stage_bytes_t(int R) {
   return (128 + DEST_CL * R * 128 + DeStCfg<NW, J>::GI_BYTES + 127) & ~127;
 }
-// Largest GI block of the configurations below (sizes the two-stage check).
-int de_stage_bytes(int R) { return de_stage_bytes_t<11, 17>(R); }
+constexpr int DEST_NW = 15, DEST_J = 12;   // 720 vocab rows x 64 columns per CTA (128 regs)
+int de_stage_bytes(int R) { return de_stage_bytes_t<DEST_NW, DEST_J>(R); }
 
 template <int NW, int J, typename OutT>
 int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
@@ -853,13 +922,11 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
 }
 
 // Register budget split between accumulators (reuse: VB vocab rows per staged
-// H tile) and loads in flight (latency hiding): 15 consumer warps x 12 rows
-// (128 regs) vs 11 x 17 (168 regs); SPARTON_DEST_CFG=1 selects the latter.
+// H tile) and loads in flight (latency hiding): 15 consumer warps x 12 rows at
+// 128 registers measured 7% faster than 11 x 17 at 168.
 template <typename OutT>
 int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
-  const char* ev = getenv("SPARTON_DEST_CFG");
-  if (ev && ev[0] == '1') return launch_de_staged_t<11, 17, OutT>(p, tmH, stream);
-  return launch_de_staged_t<15, 12, OutT>(p, tmH, stream);
+  return launch_de_staged_t<DEST_NW, DEST_J, OutT>(p, tmH, stream);
 }
 
 template <int CPL, int W, typename OutT>
@@ -976,6 +1043,7 @@ BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long lo
   long long wpc = chunk_bytes / ((long long)RT_WIN * D * 2);
   if (wpc < 1) wpc = 1;
   if (wpc > w.nwin) wpc = w.nwin;
+  if (wpc > 32) wpc = 32;                    // dH reads one pass's window bounds with one warp
   w.wpc = (int)wpc;
   w.nchunks = (w.nwin + w.wpc - 1) / w.wpc;
   w.pairs = 0;

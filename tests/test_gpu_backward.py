@@ -69,7 +69,9 @@ def test_golden_backward(cuda_device, name):
 GRID = [(1, 1, 16, 1), (2, 3, 16, 5), (4, 8, 16, 16), (2, 64, 64, 300), (3, 130, 256, 389),
         (2, 512, 768, 2000), (4, 33, 1024, 777), (2, 40, 520, 100), (3, 7, 8, 1000),
         # S beyond the staged dE's two-stage smem limit: the gathered dE path.
-        (2, 1000, 128, 700), (5, 856, 64, 1501)]
+        (2, 1000, 128, 700), (5, 856, 64, 1501),
+        # S > 2125: fewer than 16 route segments fit in smem (two-pass route)
+        (1, 2200, 16, 3000)]
 
 
 @pytest.mark.parametrize("dims", GRID)
