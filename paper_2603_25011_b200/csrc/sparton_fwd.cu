@@ -131,6 +131,48 @@ __device__ __forceinline__ void reduce_group(const float (&r)[32], float nbias, 
   }
 }
 
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// Unmasked 32-column group, fewer instructions per logit than reduce_group:
+// the group maximum m comes from a three-input max tree (block maxima of 8
+// columns first); only when some lane of the warp improves its running best
+// (m > best) does the warp locate the first column equal to m — first the
+// block (reverse select over the 4 block maxima), then the column inside the
+// block (the block's 8 values gathered by two select levels, reverse select).
+// Same result as the strict '>' scan: first occurrence of the maximum.
+__device__ __forceinline__ void reduce_group_fast(const float (&r)[32], int c0, float& best, int& bidx) {
+  float bm[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float* x = r + 8 * k;
+    bm[k] = max3f(max3f(x[0], x[1], x[2]), max3f(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
+  }
+  const float m = max3f(bm[0], bm[1], fmaxf(bm[2], bm[3]));
+  const bool better = m > best;
+  if (__any_sync(0xffffffffu, better)) {
+    int kb = 3;
+    kb = (bm[2] == m) ? 2 : kb;
+    kb = (bm[1] == m) ? 1 : kb;
+    kb = (bm[0] == m) ? 0 : kb;
+    const bool lo = (kb & 1) != 0, hi = (kb & 2) != 0;
+    int kk = 7;
+#pragma unroll
+    for (int k = 6; k >= 0; --k) {
+      const float t0 = lo ? r[8 + k] : r[k];
+      const float t1 = lo ? r[24 + k] : r[16 + k];
+      kk = ((hi ? t1 : t0) == m) ? k : kk;
+    }
+    if (better) {
+      best = m;
+      bidx = c0 + 8 * kb + kk;
+    }
+  }
+}
+
 template <int CG, int NP>
 __global__ void __launch_bounds__(FwdCfg<CG, NP>::NUM_THREADS, 1)
 sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmH,
@@ -336,6 +378,8 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           } else if (p.epi_mode == 3) {
 #pragma unroll
             for (int c = 0; c < 32; ++c) if (r[c] > cb[c & 3]) cb[c & 3] = r[c];
+          } else if (keep[j] == 0xffffffffu && p.epi_mode != 4) {
+            reduce_group_fast(r, j * 32, cb[0], ci[0]);
           } else if ((keep[j] | zero[j]) != 0u) {
             reduce_group(r, -bv, keep[j], zero[j], j * 32, cb, ci);
           }
