@@ -378,10 +378,19 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           } else if (p.epi_mode == 3) {
 #pragma unroll
             for (int c = 0; c < 32; ++c) if (r[c] > cb[c & 3]) cb[c & 3] = r[c];
-          } else if (keep[j] == 0xffffffffu && p.epi_mode != 4) {
+          } else if (p.epi_mode == 4) {   // experiment switch: the per-element strict '>' scan
+            if ((keep[j] | zero[j]) != 0u) reduce_group(r, -bv, keep[j], zero[j], j * 32, cb, ci);
+          } else if (keep[j] == 0xffffffffu) {
             reduce_group_fast(r, j * 32, cb[0], ci[0]);
           } else if ((keep[j] | zero[j]) != 0u) {
-            reduce_group(r, -bv, keep[j], zero[j], j * 32, cb, ci);
+            // Masked / ragged group: substitute the competing raw values first
+            // (masked -> -bias, i.e. logit 0; beyond S -> -inf), then reduce.
+            const uint32_t kp = keep[j], zr = zero[j];
+            const float nb = -bv;
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              r[c] = ((kp >> c) & 1u) ? r[c] : (((zr >> c) & 1u) ? nb : -INFINITY);
+            reduce_group_fast(r, j * 32, cb[0], ci[0]);
           }
         }
         // Accumulator fully read: hand it back to the MMA warp.
