@@ -357,7 +357,7 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* m, uint32_t ds
 template <int NW, int J, typename OutT>
 __global__ void __launch_bounds__(DeStCfg<NW, J>::THREADS, 1)
 sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdParams p, int R, int nst,
-                             int stage_bytes) {
+                             int stage_bytes, int nvg, int nitems) {
   using C = DeStCfg<NW, J>;
   extern __shared__ __align__(128) uint8_t ds_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(ds_smem + (size_t)nst * stage_bytes);
@@ -365,8 +365,10 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = ptx::cluster_ctarank();
-  const int v0 = blockIdx.x * C::VB;
-  const int d0 = blockIdx.y * DEST_DD;
+  // Persistent: cluster c walks work items c, c + G, ... ; item i = (vocab
+  // group i % nvg of DEST_CL blocks, D slice i / nvg).  Consecutive clusters
+  // share a D slice, so their H tiles are L2-shared.
+  const int cl = (int)(blockIdx.x / DEST_CL), ncl = (int)(gridDim.x / DEST_CL);
   // Stage layout: [zero row][S-row tile][GI records].  s = -1 (inactive pair)
   // addresses the zero row, so inactive pairs never touch H.
   const uint32_t tile_bytes = (uint32_t)(DEST_CL * R * 128);
@@ -394,10 +396,13 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
     if (lane == 0) {
       // ------------------------------------------------ producer
       const uint64_t pol = ptx::policy_evict_normal();
-      const long long vrem = (long long)p.ldGI - v0;          // even
-      const uint32_t gi_bytes = (uint32_t)(vrem >= C::VB ? C::GI_BYTES : (vrem > 0 ? vrem * 8 : 0));
       int st = 0;
       uint32_t ph = 0;
+      for (int it = cl; it < nitems; it += ncl) {
+      const int v0 = ((it % nvg) * DEST_CL + (int)crank) * C::VB;
+      const int d0 = (it / nvg) * DEST_DD;
+      const long long vrem = (long long)p.ldGI - v0;          // even
+      const uint32_t gi_bytes = (uint32_t)(vrem >= C::VB ? C::GI_BYTES : (vrem > 0 ? vrem * 8 : 0));
       for (int b = 0; b < p.B; ++b) {
         ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
         const uint32_t sbase = ptx::smem_u32(ds_smem + (size_t)st * stage_bytes);
@@ -408,19 +413,23 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
         if (gi_bytes) bulk_g2s(sbase + gi_off, p.gi + (size_t)b * p.ldGI + v0, gi_bytes, fb);
         if (++st == nst) { st = 0; ph ^= 1; }
       }
+      }
     }
     __syncwarp();
   } else {
     // ------------------------------------------------ consumers
     const int grp = warp * 4 + (lane >> 3);
     const int sub = lane & 7;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = cl; it < nitems; it += ncl) {
+    const int v0 = ((it % nvg) * DEST_CL + (int)crank) * C::VB;
+    const int d0 = (it / nvg) * DEST_DD;
     float acc[J][8];
 #pragma unroll
     for (int j = 0; j < J; ++j)
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
-    int st = 0;
-    uint32_t ph = 0;
     for (int b = 0; b < p.B; ++b) {
       ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
       const uint8_t* tile = ds_smem + (size_t)st * stage_bytes;
@@ -448,6 +457,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
         if (v < p.V) store8<OutT>(reinterpret_cast<OutT*>(p.dE) + (size_t)v * p.D + d, acc[j]);
       }
     }
+    }  // items
   }
   // Peers may still multicast into / arrive on this CTA until every CTA is done.
   ptx::cluster_sync();
@@ -901,8 +911,15 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de_staged)", e);
   const int nvb = (p.V + C::VB - 1) / C::VB;
+  const int nvg = (nvb + DEST_CL - 1) / DEST_CL;
+  const int nitems = nvg * ((p.D + DEST_DD - 1) / DEST_DD);
+  int ncl = nitems;
+  if (const char* ev = getenv("SPARTON_DE_CLUSTERS")) {   // persistent grid (SM partition experiments)
+    const int n = atoi(ev);
+    if (n > 0 && n < ncl) ncl = n;
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((nvb + DEST_CL - 1) / DEST_CL * DEST_CL), (unsigned)((p.D + DEST_DD - 1) / DEST_DD), 1);
+  cfg.gridDim = dim3((unsigned)(ncl * DEST_CL), 1, 1);
   cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -913,7 +930,7 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, *tmH, p, R, nst, stage_bytes);
+  e = cudaLaunchKernelEx(&cfg, kern, *tmH, p, R, nst, stage_bytes, nvg, nitems);
   if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_de_staged_kernel", e);
   sparton_bwd_db_kernel<<<(p.V + 255) / 256, 256, 0, stream>>>(p);
   e = cudaGetLastError();
@@ -960,35 +977,10 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
       if ((rc = launch_de_staged<OutT>(p, tmH, stream)) != SPARTON_OK) return rc;
       return launch_dh<CPL, OutT>(p, stream);
     }
-    if (mode == 5) {   // dH first (persistent grid grabs its SMs), then dE on the side stream
-      static cudaEvent_t ev[5];
-      static bool init = false;
-      const bool dbg = getenv("SPARTON_BWD_EVENTS") != nullptr;
-      if (dbg && !init) { for (auto& x : ev) cudaEventCreate(&x); init = true; }
-      if (dbg) cudaEventRecord(ev[0], stream);
-      if ((rc = fork()) != SPARTON_OK) return rc;
-      if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
-      if (dbg) { cudaEventRecord(ev[1], stream); cudaEventRecord(ev[2], ss.s); }
-      if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
-      if (dbg) cudaEventRecord(ev[3], ss.s);
-      rc = join();
-      if (dbg) {
-        cudaEventSynchronize(ev[3]);
-        cudaEventSynchronize(ev[1]);
-        float a, b, c;
-        cudaEventElapsedTime(&a, ev[0], ev[1]);
-        cudaEventElapsedTime(&b, ev[0], ev[2]);
-        cudaEventElapsedTime(&c, ev[0], ev[3]);
-        fprintf(stderr, "bwd events: dH end %.2f  dE start %.2f  dE end %.2f ms\n", a, b, c);
-      }
-      return rc;
-    }
-    if (mode == 6) {   // experiment: dH then dE, one stream
-      if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
-      return launch_de_staged<OutT>(p, tmH, stream);
-    }
-    if (mode == 3) return launch_de_staged<OutT>(p, tmH, stream);   // experiment: dE only
-    if (mode == 4) return launch_dh<CPL, OutT>(p, stream);          // experiment: dH only
+    // Timing experiments only (tools/bwd_parts.py): one gradient family, the
+    // others left unwritten — so they also require SPARTON_ALLOW_PARTIAL_BWD=1.
+    if ((mode == 3 || mode == 4) && getenv("SPARTON_ALLOW_PARTIAL_BWD") != nullptr)
+      return mode == 3 ? launch_de_staged<OutT>(p, tmH, stream) : launch_dh<CPL, OutT>(p, stream);
     if ((rc = fork()) != SPARTON_OK) return rc;
     if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
     if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
