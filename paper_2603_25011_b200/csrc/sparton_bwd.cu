@@ -867,8 +867,9 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
     if (n > 0 && n < gx) gx = n;
   }
   dim3 grid((unsigned)gx, dslices);
-  // 2 E rows in flight per warp at 4 CTAs (32 warps) per SM measured best
-  // (1.34 ms/pass at cfg3) against 4 rows x 2 CTAs, 3 x 3 and D-sliced variants.
+  // 3 E rows in flight per warp at 3 CTAs (24 warps) per SM measured 2.4 %
+  // faster than 2 x 4 and 4 x 2 (tools/ab_dh.sh, locked clocks); bypassing L1
+  // for the gathered rows (ld.global.nc.L1::no_allocate) was 56 % slower.
   const bool full = p.D % (256 * CPL) == 0;
   if (const char* ev = getenv("SPARTON_DH_FAT")) {   // experiment: n persistent 1024-thread CTAs (1 per SM)
     const int n = atoi(ev);
@@ -882,7 +883,7 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
     }
   }
   for (int c = 0; c < p.nchunks; ++c) {
-    if (full) sparton_bwd_dh_kernel<CPL, 2, 4, true, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
+    if (full) sparton_bwd_dh_kernel<CPL, 3, 3, true, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
     else sparton_bwd_dh_kernel<CPL, 2, 4, false, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
