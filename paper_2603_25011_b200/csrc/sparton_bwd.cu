@@ -11,31 +11,33 @@
 // every output element has exactly one owner that accumulates in the
 // reference's order — b ascending for dE/db, v ascending for dH.
 //
-//   K2s sparton_bwd_de_staged_kernel (S <= 856, the default): CTA owns 748
+//   K2s sparton_bwd_de_staged_kernel (S <= 856, the default): CTA owns 720
 //                               vocab rows x 64 columns of D with fp32 sums in
 //                               registers over the whole batch; per batch row
 //                               the H[b] slice is staged in smem (TMA multicast
 //                               over a 4-CTA cluster) and every pair reads its
 //                               argmax row from smem.  db by a column-sum kernel.
-//   K2 sparton_bwd_de_kernel  : (S > 856) CTA owns 32 vocab rows x one D slice; warps own
-//                               4 vocab rows, lanes 8-wide D chunks; for each
+//   K2 sparton_bwd_de_kernel  : (S > 856) CTA owns 2*W vocab rows x one D slice; warps own
+//                               2 vocab rows, lanes 8-wide D chunks; for each
 //                               batch row (ascending) each warp gathers its
 //                               argmax H rows with 1-D TMA bulk copies into a
 //                               private mbarrier ring, 4 batch rows deep.
-//   K3a sparton_bwd_route_kernel : CTA per (vocab window, b): a stable counting
-//                               sort in smem of the window's active (v, g) pairs
-//                               by argmax position s, written out coalesced as
-//                               per-(b, window, s) lists in ascending v.
+//   K3a sparton_bwd_route_kernel : CTA per (vocab window, b): one pass over Y/I/dY
+//                               computes g and the staged dE's (s, g) records,
+//                               then a stable counting sort in smem of the
+//                               window's active (v, g) pairs by argmax position
+//                               s, written out coalesced as per-(b, window, s)
+//                               lists in ascending v.
 //   K3b sparton_bwd_dh_kernel : warp owns one (b, s) row (x D slice) and sums
 //                               g * E[v,:] over its list in ascending v, in
-//                               L2-sized vocabulary chunks (one launch each).
+//                               L2-sized vocabulary chunks (one launch each,
+//                               the fp32 partial sums carried between them).
 // All arithmetic is fp32 (inputs bf16), exactly one owner per output element.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
-#include <cstdio>
 #include <mutex>
 
 #include "ptx.cuh"

@@ -190,10 +190,11 @@ def test_deterministic_run_to_run(cuda_device):
 
 # ---------------------------------------------------------------- full-size configs via B-slices
 
-@pytest.mark.parametrize("V", [30522, 250002])
-def test_fullsize_rows_vs_oracle(cuda_device, V):
+@pytest.mark.parametrize("V,ragged", [(30522, False), (250002, False), (30522, True)])
+def test_fullsize_rows_vs_oracle(cuda_device, V, ragged):
     """cfg2 / cfg3 shapes (B=S=512, D=768): the head is separable in b, so the
-    oracle on 2 sampled batch rows reproduces those rows exactly."""
+    oracle on 2 sampled batch rows reproduces those rows exactly.  The ragged
+    case pads every row to a random length and adds a bias (masked epilogue)."""
     B, S, D = 512, 512, 768
     gen = torch.Generator(device="cuda").manual_seed(0)
     dev = torch.device("cuda", 0)
@@ -201,6 +202,10 @@ def test_fullsize_rows_vs_oracle(cuda_device, V):
     E = (torch.randn((V, D), generator=gen, device=dev) * 0.02).to(torch.bfloat16)
     b = torch.zeros(V, device=dev)
     m = torch.ones((B, S), dtype=torch.uint8, device=dev)
+    if ragged:
+        b = torch.randn(V, generator=gen, device=dev) * 0.1
+        lens = torch.randint(1, S + 1, (B,), generator=gen, device=dev)
+        m = (torch.arange(S, device=dev)[None] < lens[:, None]).to(torch.uint8)
     Y, I = _head()(H, E, b, m)
     torch.cuda.synchronize()
     rows = [0, 311]

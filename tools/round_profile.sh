@@ -12,3 +12,6 @@ timeout 300 python bench.py --config cfg2 --steps 10 --warmup 3 > gpurun_out/ben
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.txt 2>&1
 timeout 600 python tools/naive_bench.py > gpurun_out/naive.txt 2>&1
 tail -1 gpurun_out/bench_cfg3_full.txt; tail -1 gpurun_out/bench_cfg2_full.txt; tail -1 gpurun_out/bench_ref.txt; tail -3 gpurun_out/naive.txt
+timeout 900 python tools/splade_bench.py 64 256 > gpurun_out/splade.txt 2>&1
+timeout 300 python bench.py --config cfg4 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_cfg4.txt 2>&1
+tail -1 gpurun_out/bench_cfg4.txt
