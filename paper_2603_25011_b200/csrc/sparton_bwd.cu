@@ -981,8 +981,8 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
       return launch_dh<CPL, OutT>(p, stream);
     }
     // Timing experiments only (tools/bwd_parts.py): one gradient family, the
-    // others left unwritten — so they also require SPARTON_ALLOW_PARTIAL_BWD=1.
-    if ((mode == 3 || mode == 4) && getenv("SPARTON_ALLOW_PARTIAL_BWD") != nullptr)
+    // others left unwritten — so they also require SPARTON_EXPERIMENTS=1.
+    if ((mode == 3 || mode == 4) && getenv("SPARTON_EXPERIMENTS") != nullptr)
       return mode == 3 ? launch_de_staged<OutT>(p, tmH, stream) : launch_dh<CPL, OutT>(p, stream);
     if ((rc = fork()) != SPARTON_OK) return rc;
     if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;

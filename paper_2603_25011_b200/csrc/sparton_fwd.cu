@@ -501,8 +501,11 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   if (gv < 1) gv = 1;
   if (gv > prm.num_vt) gv = prm.num_vt;
   prm.group_vt = gv;
+  // Epilogue experiment switch (1-3: max-only variants with WRONG I, 4: the
+  // per-element strict '>' scan) — honoured only with SPARTON_EXPERIMENTS=1.
   prm.epi_mode = 0;
-  if (const char* ev = getenv("SPARTON_FWD_EPI")) prm.epi_mode = atoi(ev);
+  if (const char* ev = getenv("SPARTON_FWD_EPI"))
+    if (getenv("SPARTON_EXPERIMENTS") != nullptr) prm.epi_mode = atoi(ev);
   prm.sched_bgroups = 0;   // measured: the grouped round-robin moves less DRAM (profiles/)
   if (const char* ev = getenv("SPARTON_FWD_SCHED")) prm.sched_bgroups = ev[0] == '1';
   int rot = (int)(0.618 * nclusters + 0.5);

@@ -1,4 +1,5 @@
 """Time the fused forward at a shape (CUDA events, 10 iters after 3 warm-ups): ms and TF/s."""
+import os
 import subprocess
 import sys
 import time
@@ -6,6 +7,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2603_25011_b200 import sparton_forward
 
+os.environ.setdefault("SPARTON_EXPERIMENTS", "1")   # lets SPARTON_FWD_EPI experiments through
 B, S, D, V = (int(x) for x in sys.argv[1:5])
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(0)
