@@ -301,7 +301,9 @@ def run_gpu_arm(args, c, cname):
                      "frac": achieved / peaks["bf16_tflops_sustained"],
                      "frac_of_burst": achieved / peaks["bf16_tflops"],
                      "traffic": ncu_traffic(cname), "algorithmic_flops_per_launch": fwd_flops_rank,
-                     "peak_source": peaks["source"] + " (sustained; burst in frac_of_burst)"},
+                     "peak_source": peaks["source"] + " (sustained: K1 runs inside a long step; burst in "
+                                    "frac_of_burst. frac > 1 means the step's lighter backward phase lets the "
+                                    "forward hold higher clocks than a back-to-back cuBLAS loop at the power cap)"},
         "gpu_launches": launches_per_step(c, v1 - v0) * args.steps,
         "clocks": clocks,
     }
