@@ -222,3 +222,18 @@ def test_de_paths_agree(cuda_device, monkeypatch, dims, grad_dtype):
     ga = run_bwd(H, E, Y, I, dY, grad_dtype=grad_dtype)
     for x, y in zip(st, ga):
         assert np.array_equal(x, y)
+
+
+def test_persistent_de_grid_bitwise_equal(cuda_device, monkeypatch):
+    """The staged dE with a persistent grid (clusters walking several work items,
+    SPARTON_DE_CLUSTERS) produces exactly the one-item-per-cluster result."""
+    B, S, D, V = 3, 100, 192, 4000
+    H, E, b, m = orc.seeded_inputs(B, S, D, V, 61, mask_keep=0.9)
+    H, E = orc.bf16_round(H), orc.bf16_round(E)
+    dY = orc.seeded_uniform((B, V), 62)
+    Y, I = run_fwd(H, E, b, m)
+    ref = run_bwd(H, E, Y, I, dY)
+    monkeypatch.setenv("SPARTON_DE_CLUSTERS", "2")
+    got = run_bwd(H, E, Y, I, dY)
+    for x, y in zip(ref, got):
+        assert np.array_equal(x, y)
