@@ -88,3 +88,12 @@ def test_shard_ranges_partition_vocab(V, P):
     assert Vp * P >= V
     with pytest.raises(ValueError):
         shard_range(V, P, P)
+
+
+def test_sweep_rejects_bad_axis_and_empty_values():
+    from paper_2603_25011_b200 import sweep
+    with pytest.raises(ValueError):
+        sweep.run_sweep((2, 3, 8, 5), "Q", [1])
+    with pytest.raises(ValueError):
+        sweep.run_sweep((2, 3, 8, 5), "V", [])
+    assert sweep.main(["--base", "1,2,3"]) == 2

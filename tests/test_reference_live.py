@@ -60,3 +60,14 @@ def test_mirror_api_types_match_reference(fh):
         c1 = mine.TileConfig.default_for(mine.Dims(*dims))
         c2 = fh.TileConfig.default_for(fh.Dims(*dims))
         assert (c1.vocab_tile, c1.batch_tile) == (c2.vocab_tile, c2.batch_tile)
+
+
+def test_sweep_csv_schema_matches_reference(fh):
+    # The GPU sweep keeps the reference harness's CSV columns (bench.py:32-35)
+    # and checksum (bench.py:61-62), then appends its GPU columns.
+    from fusedhead import bench as ref_bench
+    from paper_2603_25011_b200 import sweep
+    assert sweep.REFERENCE_HEADER == ref_bench.BENCH_CSV_HEADER
+    assert sweep.HEADER.startswith(ref_bench.BENCH_CSV_HEADER + ",")
+    Y = np.random.default_rng(0).random((3, 7), dtype=np.float32)
+    assert sweep.y_checksum(Y) == ref_bench.y_checksum(Y)
