@@ -74,7 +74,7 @@ struct UnitIter {
       // clusters share H[b] and the group's E tiles stay L2-resident.
       // (num_units < 2^31 is checked on the host: 32-bit index math.)
       if (u >= (unsigned)p.num_units) return false;
-      const unsigned per_group = (unsigned)p.group_vt * (unsigned)p.B;
+      const unsigned per_group = (unsigned)p.group_vt * (unsigned)p.urows;
       const unsigned gg = u / per_group;
       const unsigned r = u - gg * per_group;
       const int gv0 = (int)gg * p.group_vt;
@@ -90,7 +90,7 @@ struct UnitIter {
       if (g0 >= p.num_vt) return false;
       const int gsz = min(p.group_vt, p.num_vt - g0);
       const int bb = j * nc + (int)(((long long)c + (long long)g * p.rot) % nc);
-      if (bb < p.B) {
+      if (bb < p.urows) {
         b = bb;
         vt = g0 + k;
         if (++k == gsz) { k = 0; ++j; }
@@ -244,7 +244,9 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     while (it.next(p, b, vt)) {
       const int vrow = vt * C::TILE_V + (int)pair * (C::BM * CG) + (int)rank * C::BM;
       for (int sc = 0; sc < nsc; ++sc) {
-        const int hrow = b * p.S + sc * C::SN + (int)rank * C::BN_CTA + (int)pair * C::BN_LOAD;
+        // Packed short sequences: unit row b is the batch-row group b*pack .. b*pack+pack-1,
+        // whose pack*S = 256 positions are contiguous rows of H.
+        const int hrow = b * p.pack * p.S + sc * C::SN + (int)rank * C::BN_CTA + (int)pair * C::BN_LOAD;
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
           if (ptx::elect_one()) {
@@ -333,6 +335,57 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     while (it.next(p, b, vt)) {
       const int v = vt * C::TILE_V + (int)pair * (C::BM * CG) + (int)rank * C::BM + row;
       const float bv = (v < p.V) ? __ldg(p.bias + v) : 0.0f;
+      if (p.pack > 1) {
+        // ---- packed chunk: pack batch rows of S = 256/pack positions; each
+        // 32-column group belongs to one batch row (S is a multiple of 32).
+        const int gps = p.S >> 5;                   // groups per batch row
+        ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), aph);
+        ptx::tc_fence_after();
+        const uint32_t tacc = tq + (uint32_t)(acc * C::SN);
+        float cbest = -INFINITY;
+        int cidx = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int seg = j / gps, jj = j - seg * gps;
+          const int bb = b * p.pack + seg;
+          const bool brow = bb < p.B;
+          const uint32_t keep = __ballot_sync(0xffffffffu,
+                                              brow && __ldg(p.mask + (size_t)(brow ? bb : 0) * p.S + jj * 32 + lane) != 0);
+          const uint32_t zero = brow ? ~keep : 0u;
+          float r[32];
+          ptx::tmem_ld32(tacc + (uint32_t)(j * 32), r);
+          ptx::tmem_ld_wait();
+          ptx::reg_fence32(r);
+          if (keep == 0xffffffffu) {
+            reduce_group_fast(r, jj * 32, cbest, cidx);
+          } else if ((keep | zero) != 0u) {
+            const float nb = -bv;
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              r[c] = ((keep >> c) & 1u) ? r[c] : (((zero >> c) & 1u) ? nb : -INFINITY);
+            reduce_group_fast(r, jj * 32, cbest, cidx);
+          }
+          if (jj == gps - 1) {                      // batch row complete
+            if (brow && v < p.V) {
+              const size_t o = (size_t)bb * (size_t)p.ldY + (size_t)v;
+              p.Y[o] = log1pf(fmaxf(cbest + bv, 0.0f));
+              p.I[o] = cidx;
+            }
+            cbest = -INFINITY;
+            cidx = 0;
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t te = acc ? tempty1 : tempty0;
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster_relaxed(te);
+          else ptx::mbar_arrive(te);
+        }
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+        continue;
+      }
       const uint8_t* mrow = p.mask + (size_t)b * p.S;
       float best = -INFINITY;
       int bidx = 0;
@@ -488,7 +541,12 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
                int num_sms, cudaStream_t stream) {
   const int tile_v = 128 * cluster_ctas;
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
-  prm.num_units = (long long)prm.num_vt * prm.B;
+  // Short sequences (S = 32, 64, 128): pack 256/S batch rows into one 256-column
+  // chunk so the MMA computes no padding columns (SPLADE queries).
+  prm.pack = (prm.S == 32 || prm.S == 64 || prm.S == 128) ? 256 / prm.S : 1;
+  if (const char* ev = getenv("SPARTON_FWD_PACK")) if (ev[0] == '0') prm.pack = 1;
+  prm.urows = (prm.B + prm.pack - 1) / prm.pack;
+  prm.num_units = (long long)prm.num_vt * prm.urows;
   if (prm.num_units >= (1ll << 31) - 4096)
     return set_error(SPARTON_EINVAL, "B * ceil(V / vocab_tile) exceeds the forward scheduler's 31-bit unit index");
   const int nclusters = max(1, num_sms / cluster_ctas);

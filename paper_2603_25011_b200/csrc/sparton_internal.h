@@ -25,6 +25,8 @@ struct FwdParams {
   int sched_bgroups;   // 1: batch-row-per-cluster groups (large B), 0: round-robin units
   int rot;             // per-group rotation of the cluster -> batch-row assignment
   int epi_mode;        // experiment switch: 1 = max-only epilogue (no bias/argmax; wrong I)
+  int pack;            // batch rows per 256-position chunk (S = 256/pack in {32, 64, 128}), else 1
+  int urows;           // unit rows: B (pack == 1) or ceil(B / pack) batch-row groups
 };
 
 struct BwdParams {

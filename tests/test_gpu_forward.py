@@ -221,3 +221,27 @@ def test_fullsize_rows_vs_oracle(cuda_device, V, ragged):
     # properties over the whole output
     assert torch.isfinite(Y).all() and (Y >= 0).all()
     assert int(I.min()) >= 0 and int(I.max()) < S
+
+
+@pytest.mark.parametrize("dims", [(3, 32, 64, 700), (9, 64, 128, 2000), (5, 128, 256, 1500), (17, 32, 768, 999)])
+@pytest.mark.parametrize("cg", [2, 1])
+def test_packed_short_sequences_vs_oracle(cuda_device, dims, cg):
+    """S in {32, 64, 128}: 256/S batch rows share one 256-column chunk (B not a
+    multiple of the pack, ragged masks, a fully masked row, bias)."""
+    B, S, D, V = dims
+    H, E, b, m = orc.seeded_inputs(B, S, D, V, 70 + S, mask_keep=0.8)
+    H, E = orc.bf16_round(H), orc.bf16_round(E)
+    m[0, :] = 0
+    Yg, Ig = run_fwd(H, E, b, m, cta_group=cg)
+    Yr, Ir = orc.forward(H, E, b, m)
+    assert_parity(H, E, b, m, Yg, Ig, Yr, Ir)
+
+
+def test_packed_equals_unpacked_bitwise(cuda_device, monkeypatch):
+    B, S, D, V = 7, 64, 192, 1300
+    H, E, b, m = orc.seeded_inputs(B, S, D, V, 81, mask_keep=0.9)
+    H, E = orc.bf16_round(H), orc.bf16_round(E)
+    Y1, I1 = run_fwd(H, E, b, m)
+    monkeypatch.setenv("SPARTON_FWD_PACK", "0")
+    Y0, I0 = run_fwd(H, E, b, m)
+    assert np.array_equal(Y1, Y0) and np.array_equal(I1, I0)
