@@ -703,8 +703,10 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       if (dvalid[c]) {
-        const float4 a = *reinterpret_cast<const float4*>(src + c * 256);
-        const float4 bq = *reinterpret_cast<const float4*>(src + c * 256 + 4);
+        // The fp32 carry streams through once per pass: evict-first so it does
+        // not push the pass's E chunk out of L2.
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(src + c * 256));
+        const float4 bq = __ldcs(reinterpret_cast<const float4*>(src + c * 256 + 4));
         acc[c * 8 + 0] = a.x; acc[c * 8 + 1] = a.y; acc[c * 8 + 2] = a.z; acc[c * 8 + 3] = a.w;
         acc[c * 8 + 4] = bq.x; acc[c * 8 + 5] = bq.y; acc[c * 8 + 6] = bq.z; acc[c * 8 + 7] = bq.w;
       } else {
@@ -788,7 +790,11 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
     float* dst = accg + (size_t)rowid * p.D + d0 + lane * 8;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
-      if (dvalid[c]) store8<float>(dst + c * 256, &acc[c * 8]);
+      if (dvalid[c]) {
+        __stcs(reinterpret_cast<float4*>(dst + c * 256), make_float4(acc[c * 8], acc[c * 8 + 1], acc[c * 8 + 2], acc[c * 8 + 3]));
+        __stcs(reinterpret_cast<float4*>(dst + c * 256 + 4),
+               make_float4(acc[c * 8 + 4], acc[c * 8 + 5], acc[c * 8 + 6], acc[c * 8 + 7]));
+      }
   }
   }  // rows
 }
