@@ -246,7 +246,10 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       for (int sc = 0; sc < nsc; ++sc) {
         // Packed short sequences: unit row b is the batch-row group b*pack .. b*pack+pack-1,
         // whose pack*S = 256 positions are contiguous rows of H.
-        const int hrow = b * p.pack * p.S + sc * C::SN + (int)rank * C::BN_CTA + (int)pair * C::BN_LOAD;
+        // The last chunk of a unit may be narrower (p.n_last columns): the CTA
+        // pair then splits those columns evenly, so CTA 1's rows start at n_last/2.
+        const int half = (NP == 1 && sc == nsc - 1) ? (p.n_last >> 1) : C::BN_CTA;
+        const int hrow = b * p.pack * p.S + sc * C::SN + (int)rank * half + (int)pair * C::BN_LOAD;
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
           if (ptx::elect_one()) {
@@ -280,7 +283,9 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     if (rank == 0) {
       // ------------------------------------------------ MMA issuer
       // Warp-uniform loop; one elected lane issues the MMAs and commits.
-      constexpr uint32_t idesc = ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
+      constexpr uint32_t idesc_full = ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
+      // Narrow last chunk (S not a multiple of 256): only its columns are computed.
+      const uint32_t idesc_last = NP == 1 ? ptx::umma_idesc_bf16(C::UMMA_M, p.n_last) : idesc_full;
       int st = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -292,6 +297,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), aph ^ 1);
           ptx::tc_fence_after();
           const uint32_t dt = tmem_base + (uint32_t)(acc * C::SN);
+          const uint32_t idesc = (sc == nsc - 1) ? idesc_last : idesc_full;
           for (int kb = 0; kb < nkb; ++kb) {
             ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
             ptx::tc_fence_after();
@@ -546,6 +552,13 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   prm.pack = (prm.S == 32 || prm.S == 64 || prm.S == 128) ? 256 / prm.S : 1;
   if (const char* ev = getenv("SPARTON_FWD_PACK")) if (ev[0] == '0') prm.pack = 1;
   prm.urows = (prm.B + prm.pack - 1) / prm.pack;
+  {
+    // UMMA N of the last sequence chunk: the remaining positions rounded up to
+    // 16 (cta_group::2 N granularity); packed chunks are always full.
+    const int rem = prm.pack > 1 ? 256 : prm.S - ((prm.S - 1) / 256) * 256;
+    prm.n_last = cluster_ctas == 1 ? 256 : ((rem + 15) / 16) * 16;
+    if (const char* ev = getenv("SPARTON_FWD_NLAST")) if (ev[0] == '0') prm.n_last = 256;
+  }
   prm.num_units = (long long)prm.num_vt * prm.urows;
   if (prm.num_units >= (1ll << 31) - 4096)
     return set_error(SPARTON_EINVAL, "B * ceil(V / vocab_tile) exceeds the forward scheduler's 31-bit unit index");

@@ -27,6 +27,7 @@ struct FwdParams {
   int epi_mode;        // experiment switch: 1 = max-only epilogue (no bias/argmax; wrong I)
   int pack;            // batch rows per 256-position chunk (S = 256/pack in {32, 64, 128}), else 1
   int urows;           // unit rows: B (pack == 1) or ceil(B / pack) batch-row groups
+  int n_last;          // UMMA N of a unit's last sequence chunk (multiple of 16, <= 256)
 };
 
 struct BwdParams {
