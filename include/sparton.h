@@ -82,6 +82,24 @@ SPARTON_API int sparton_fwd(const void* H, const void* E, const float* bias, con
                 int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY,
                 int cta_group, void* stream);
 
+/*
+ * FP8 forward (the paper's future-work item):
+ * H8/E8 are e4m3 with per-tensor scales given as device scalars amax_h/amax_e
+ * (logit = amax_h/448 * amax_e/448 * H8·E8 + bias), tensor-core
+ * tcgen05.mma kind::f8f6f4 at twice the bf16 rate.  Numerics differ from the
+ * bf16/fp32 reference by the e4m3 rounding (3 mantissa bits): Y is
+ * approximate and the argmax agrees except where logits lie within the e4m3
+ * error.  D must be a multiple of 16.  Otherwise identical to sparton_fwd.
+ */
+SPARTON_API int sparton_fwd_fp8(const void* H8, const void* E8, const float* amax_h, const float* amax_e,
+                const float* bias, const uint8_t* mask, float* Y, int32_t* I,
+                int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY,
+                int cta_group, void* stream);
+
+/* Per-tensor e4m3 quantisation of n bf16 values (n a multiple of 16, 16-B
+ * aligned): amax (device f32 scalar) = max |x|, q = e4m3(x * 448 / amax). */
+SPARTON_API int sparton_quantize_e4m3(const void* x_bf16, int64_t n, void* q_e4m3, float* amax, void* stream);
+
 /* Workspace bytes sparton_bwd needs for these sizes: the argmax-routed (v, g)
  * pair lists for dH (B*V*8 bytes) and their offsets, the per-(b, v) (s, g)
  * records of the staged dE (B*V*8 bytes, S <= 856), plus an fp32 dH

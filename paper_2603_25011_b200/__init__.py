@@ -11,7 +11,8 @@ Public surface:
   * vocab-sharded multi-GPU head: ``paper_2603_25011_b200.sharded``
 """
 
-from .head import SpartonHeadFn, bwd_workspace_bytes, sparton_backward, sparton_forward, sparton_head
+from .head import (SpartonHeadFn, bwd_workspace_bytes, quantize_e4m3, sparton_backward, sparton_forward,
+                   sparton_forward_fp8, sparton_head)
 
 __version__ = "0.1.0"
 
@@ -20,5 +21,7 @@ __all__ = [
     "bwd_workspace_bytes",
     "sparton_backward",
     "sparton_forward",
+    "sparton_forward_fp8",
+    "quantize_e4m3",
     "sparton_head",
 ]

@@ -32,6 +32,8 @@ EXPORTED = (
     "sparton_last_error",
     "sparton_device_sm_count",
     "sparton_fwd",
+    "sparton_fwd_fp8",
+    "sparton_quantize_e4m3",
     "sparton_bwd_workspace_bytes",
     "sparton_bwd",
 )
@@ -67,6 +69,11 @@ def load() -> ctypes.CDLL:
         lib.sparton_fwd.restype = c_int
         lib.sparton_fwd.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                     c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]
+        lib.sparton_fwd_fp8.restype = c_int
+        lib.sparton_fwd_fp8.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                        c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]
+        lib.sparton_quantize_e4m3.restype = c_int
+        lib.sparton_quantize_e4m3.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp]
         lib.sparton_bwd_workspace_bytes.restype = ctypes.c_size_t
         lib.sparton_bwd_workspace_bytes.argtypes = [c_i64, c_i64, c_i64, c_i64, c_int]
         lib.sparton_bwd.restype = c_int

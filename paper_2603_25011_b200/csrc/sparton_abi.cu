@@ -63,15 +63,16 @@ int device_info(DevInfo& out) {
   return SPARTON_OK;
 }
 
-int encode_bf16_2d_swz(CUtensorMap* map, const void* ptr, long long rows, long long cols,
-                       int box_rows, int box_cols, CUtensorMapSwizzle swz) {
+int encode_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, int box_rows, int box_cols,
+              CUtensorMapSwizzle swz, bool u8) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return set_error(SPARTON_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * (u8 ? 1 : 2)};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = fn(map, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(ptr), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -83,10 +84,11 @@ int encode_bf16_2d_swz(CUtensorMap* map, const void* ptr, long long rows, long l
   return SPARTON_OK;
 }
 
-int encode_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols,
-                   int box_rows, int box_cols) {
-  return encode_bf16_2d_swz(map, ptr, rows, cols, box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_128B);
+int encode_bf16_2d_swz(CUtensorMap* map, const void* ptr, long long rows, long long cols,
+                       int box_rows, int box_cols, CUtensorMapSwizzle swz) {
+  return encode_2d(map, ptr, rows, cols, box_rows, box_cols, swz, false);
 }
+
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -160,36 +162,43 @@ static int check_device() {
   return SPARTON_OK;
 }
 
-int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* mask, float* Y,
-                int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int cta_group,
-                void* stream) {
+static int fwd_common(const void* H, const void* E, const float* amax_h, const float* amax_e, const float* bias,
+                      const uint8_t* mask, float* Y, int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V,
+                      int64_t ldY, int cta_group, void* stream, bool fp8) {
   int rc = check_dims(B, S, D, V);
   if (rc) return rc;
   if (!H || !E || !bias || !mask || !Y || !I) return set_error(SPARTON_EINVAL, "null pointer argument");
+  if (fp8 && (!amax_h || !amax_e)) return set_error(SPARTON_EINVAL, "null amax pointer");
+  if (fp8 && D % 16 != 0)
+    return set_error(SPARTON_EINVAL, "e4m3 operands need D to be a multiple of 16 (TMA 16-byte stride)");
   if (!aligned16(H) || !aligned16(E)) return set_error(SPARTON_EINVAL, "H and E must be 16-byte aligned");
   if (ldY < V) return set_error(SPARTON_EINVAL, "ldY must be >= V");
   if (cta_group != 0 && cta_group != 1 && cta_group != 2 && cta_group != 4)
     return set_error(SPARTON_EINVAL, "cta_group must be 0, 1, 2 or 4");
+  if (fp8 && cta_group == 4) return set_error(SPARTON_EINVAL, "the e4m3 forward supports cta_group 0, 1 or 2");
   if ((rc = check_device())) return rc;
   DevInfo d;
   device_info(d);
   int cg = cta_group;
   if (cg == 0) {
     // Default: one CTA pair per cluster.  Two pairs sharing H tiles by TMA
-    // multicast (cg = 4) cut L2 traffic by ~30 % but ran 1.6x slower at cfg3
-    // (lock-step coupling of the pairs, 4-CTA clusters leave SMs idle).
+    // multicast (cg = 4) cut L2 traffic but measured slower inside the step
+    // (lock-step coupling of the pairs).
     cg = 2;
     if (const char* ev = getenv("SPARTON_FWD_CLUSTER")) cg = atoi(ev);
     if (cg != 1 && cg != 2 && cg != 4) cg = 2;
+    if (fp8 && cg == 4) cg = 2;
   }
   if (const char* ev = getenv("SPARTON_L2_PERSIST_MB")) {
     // Experiment switch: L2 set-aside for evict_last (persisting) lines.
     static std::once_flag once;
     std::call_once(once, [ev]() { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(ev) << 20); });
   }
+  // One 128-byte swizzle row per K step: 64 bf16 or 128 e4m3 columns.
+  const int box_cols = fp8 ? 128 : 64;
   CUtensorMap tmE, tmH;
-  if ((rc = encode_bf16_2d(&tmE, E, V, D, 128, 64))) return rc;
-  if ((rc = encode_bf16_2d(&tmH, H, B * S, D, fwd_h_box_rows(cg), 64))) return rc;
+  if ((rc = encode_2d(&tmE, E, V, D, 128, box_cols, CU_TENSOR_MAP_SWIZZLE_128B, fp8))) return rc;
+  if ((rc = encode_2d(&tmH, H, B * S, D, fwd_h_box_rows(cg), box_cols, CU_TENSOR_MAP_SWIZZLE_128B, fp8))) return rc;
   FwdParams prm = {};
   prm.bias = bias;
   prm.mask = mask;
@@ -200,6 +209,9 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
   prm.D = (int)D;
   prm.V = (int)V;
   prm.ldY = ldY;
+  prm.fp8 = fp8 ? 1 : 0;
+  prm.amax_h = amax_h;
+  prm.amax_e = amax_e;
   {
     const char* ev = getenv("SPARTON_E_EVICT_LAST");
     // bits 0-1: E policy, bits 2-3: H policy (0 normal, 1 evict_last, 2 evict_first).
@@ -207,6 +219,28 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
     prm.e_evict_last = ev ? atoi(ev) : 5;
   }
   return launch_fwd(tmE, tmH, prm, cg, d.sms, static_cast<cudaStream_t>(stream));
+}
+
+int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* mask, float* Y,
+                int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int cta_group,
+                void* stream) {
+  return fwd_common(H, E, nullptr, nullptr, bias, mask, Y, I, B, S, D, V, ldY, cta_group, stream, false);
+}
+
+int sparton_fwd_fp8(const void* H8, const void* E8, const float* amax_h, const float* amax_e, const float* bias,
+                    const uint8_t* mask, float* Y, int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V,
+                    int64_t ldY, int cta_group, void* stream) {
+  return fwd_common(H8, E8, amax_h, amax_e, bias, mask, Y, I, B, S, D, V, ldY, cta_group, stream, true);
+}
+
+int sparton_quantize_e4m3(const void* x, int64_t n, void* q, float* amax, void* stream) {
+  if (n < 1) return set_error(SPARTON_EINVAL, "n must be positive");
+  if (!x || !q || !amax) return set_error(SPARTON_EINVAL, "null pointer argument");
+  if (!aligned16(x) || !aligned16(q) || n % 16 != 0)
+    return set_error(SPARTON_EINVAL, "x and q must be 16-byte aligned and n a multiple of 16");
+  int rc = check_device();
+  if (rc) return rc;
+  return launch_quantize_e4m3(x, n, q, amax, static_cast<cudaStream_t>(stream));
 }
 
 size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t D, int64_t V, int grad_dtype) {

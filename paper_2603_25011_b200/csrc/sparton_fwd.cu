@@ -29,22 +29,25 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 
 #include "ptx.cuh"
 #include "sparton_internal.h"
 
 namespace sparton {
 
-template <int CG, int NP = 1>
+template <int CG, int NP = 1, bool FP8 = false>
 struct FwdCfg {
+  static constexpr int EB = FP8 ? 1 : 2;         // operand element bytes (e4m3 / bf16)
   static constexpr int BM = 128;                 // vocab rows per CTA (TMEM lanes)
   static constexpr int TILE_V = BM * CG * NP;    // vocab rows per unit (NP pairs share H tiles)
   static constexpr int SN = 256;                 // sequence positions per chunk (UMMA N)
   static constexpr int BN_CTA = SN / CG;         // H rows each CTA holds per chunk
   static constexpr int BN_LOAD = BN_CTA / NP;    // H rows each CTA loads (and multicasts to NP CTAs)
-  static constexpr int BK = 64;                  // K per stage = one 128-B swizzle row
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN_CTA * BK * 2;
+  static constexpr int BK = 128 / EB;            // K per stage = one 128-B swizzle row
+  static constexpr int KSTEPS = 4;               // UMMA K = 16 (bf16) / 32 (e4m3): 32 B per step
+  static constexpr int A_BYTES = BM * BK * EB;
+  static constexpr int B_BYTES = BN_CTA * BK * EB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NST = CG == 1 ? 4 : 6;   // 7 stages measured 0.8% slower (tools/ab_fwd.sh)
   static constexpr int UMMA_M = BM * CG;
@@ -173,11 +176,11 @@ __device__ __forceinline__ void reduce_group_fast(const float (&r)[32], int c0, 
   }
 }
 
-template <int CG, int NP>
-__global__ void __launch_bounds__(FwdCfg<CG, NP>::NUM_THREADS, 1)
+template <int CG, int NP, bool FP8>
+__global__ void __launch_bounds__(FwdCfg<CG, NP, FP8>::NUM_THREADS, 1)
 sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmH,
                    const FwdParams p) {
-  using C = FwdCfg<CG, NP>;
+  using C = FwdCfg<CG, NP, FP8>;
   static_assert(NP == 1 || CG == 2, "H multicast across pairs needs CTA pairs");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128-B swizzle atoms.
@@ -269,7 +272,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
                 // Same H rows are needed by CTA `rank` of every pair: each loads
                 // 1/NP of them and multicasts to its counterparts.
                 const uint16_t mc = (uint16_t)(0x5555u << rank) & all_mask;   // cluster ranks rank, rank+2, ...
-                ptx::tma_load_2d_cg2_mc(&tmH, sb + pair * (C::BN_LOAD * C::BK * 2), fb, kb * C::BK, hrow, mc,
+                ptx::tma_load_2d_cg2_mc(&tmH, sb + pair * (C::BN_LOAD * C::BK * C::EB), fb, kb * C::BK, hrow, mc,
                                         pol_h);
               }
             }
@@ -283,9 +286,11 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     if (rank == 0) {
       // ------------------------------------------------ MMA issuer
       // Warp-uniform loop; one elected lane issues the MMAs and commits.
-      constexpr uint32_t idesc_full = ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
+      constexpr uint32_t idesc_full = FP8 ? ptx::umma_idesc_e4m3(C::UMMA_M, C::SN) : ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
       // Narrow last chunk (S not a multiple of 256): only its columns are computed.
-      const uint32_t idesc_last = NP == 1 ? ptx::umma_idesc_bf16(C::UMMA_M, p.n_last) : idesc_full;
+      const uint32_t idesc_last = NP == 1 ? (FP8 ? ptx::umma_idesc_e4m3(C::UMMA_M, p.n_last)
+                                                 : ptx::umma_idesc_bf16(C::UMMA_M, p.n_last))
+                                          : idesc_full;
       int st = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -306,9 +311,10 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
               const uint64_t da = ptx::umma_desc_sw128(sa);
               const uint64_t db = ptx::umma_desc_sw128(sa + C::A_BYTES);
 #pragma unroll
-              for (int k = 0; k < C::BK / 16; ++k) {
+              for (int k = 0; k < C::KSTEPS; ++k) {
                 // +32 bytes along K inside the 128-B swizzle row = +2 in the >>4 address field.
-                ptx::umma_bf16<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                if constexpr (FP8) ptx::umma_e4m3<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                else ptx::umma_bf16<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
               }
               // The stage's H half was written by every pair's producer: release it cluster-wide.
               ptx::umma_commit<CG>(ptx::smem_u32(&empty[st]), all_mask);
@@ -325,6 +331,12 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     }
   } else {
     // ------------------------------------------------ epilogue (warps 0..3)
+    // Dequantisation scale of the raw accumulator (FP8: amax_H/448 * amax_E/448).
+    float dscale = 1.0f;
+    if constexpr (FP8) {
+      const float ah = __ldg(p.amax_h), ae = __ldg(p.amax_e);
+      dscale = (ah > 0.f ? ah / 448.0f : 1.0f) * (ae > 0.f ? ae / 448.0f : 1.0f);
+    }
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
     const int row = q * 32 + (int)lane;           // vocab row within this CTA's tile
     const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
@@ -341,6 +353,11 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     while (it.next(p, b, vt)) {
       const int v = vt * C::TILE_V + (int)pair * (C::BM * CG) + (int)rank * C::BM + row;
       const float bv = (v < p.V) ? __ldg(p.bias + v) : 0.0f;
+      // Raw-space comparisons: logit = dscale * raw + bias with dscale = 1 for
+      // bf16 and the product of the two per-tensor e4m3 scales for FP8 (> 0, so
+      // the argmax is that of the raw accumulator); a masked position (logit
+      // exactly 0) competes as raw -bias / dscale.
+      const float nbv = -bv / dscale;
       if (p.pack > 1) {
         // ---- packed chunk: pack batch rows of S = 256/pack positions; each
         // 32-column group belongs to one batch row (S is a multiple of 32).
@@ -365,7 +382,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           if (keep == 0xffffffffu) {
             reduce_group_fast(r, jj * 32, cbest, cidx);
           } else if ((keep | zero) != 0u) {
-            const float nb = -bv;
+            const float nb = nbv;
 #pragma unroll
             for (int c = 0; c < 32; ++c)
               r[c] = ((keep >> c) & 1u) ? r[c] : (((zero >> c) & 1u) ? nb : -INFINITY);
@@ -374,7 +391,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           if (jj == gps - 1) {                      // batch row complete
             if (brow && v < p.V) {
               const size_t o = (size_t)bb * (size_t)p.ldY + (size_t)v;
-              p.Y[o] = log1pf(fmaxf(cbest + bv, 0.0f));
+              p.Y[o] = log1pf(fmaxf(fmaf(cbest, dscale, bv), 0.0f));
               p.I[o] = cidx;
             }
             cbest = -INFINITY;
@@ -438,14 +455,14 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
 #pragma unroll
             for (int c = 0; c < 32; ++c) if (r[c] > cb[c & 3]) cb[c & 3] = r[c];
           } else if (p.epi_mode == 4) {   // experiment switch: the per-element strict '>' scan
-            if ((keep[j] | zero[j]) != 0u) reduce_group(r, -bv, keep[j], zero[j], j * 32, cb, ci);
+            if ((keep[j] | zero[j]) != 0u) reduce_group(r, nbv, keep[j], zero[j], j * 32, cb, ci);
           } else if (keep[j] == 0xffffffffu) {
             reduce_group_fast(r, j * 32, cb[0], ci[0]);
           } else if ((keep[j] | zero[j]) != 0u) {
             // Masked / ragged group: substitute the competing raw values first
             // (masked -> -bias, i.e. logit 0; beyond S -> -inf), then reduce.
             const uint32_t kp = keep[j], zr = zero[j];
-            const float nb = -bv;
+            const float nb = nbv;
 #pragma unroll
             for (int c = 0; c < 32; ++c)
               r[c] = ((kp >> c) & 1u) ? r[c] : (((zr >> c) & 1u) ? nb : -INFINITY);
@@ -475,7 +492,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       }
       if (v < p.V) {
         const size_t o = (size_t)b * (size_t)p.ldY + (size_t)v;
-        p.Y[o] = log1pf(fmaxf(best + bv, 0.0f));
+        p.Y[o] = log1pf(fmaxf(fmaf(best, dscale, bv), 0.0f));
         p.I[o] = bidx;
       }
     }
@@ -491,12 +508,12 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
 
 // ------------------------------------------------------------------ host side
 
-template <int CG, int NP>
+template <int CG, int NP, bool FP8>
 int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdParams& prm,
                     int num_sms, cudaStream_t stream) {
-  using C = FwdCfg<CG, NP>;
+  using C = FwdCfg<CG, NP, FP8>;
   constexpr int CL = CG * NP;   // cluster size
-  auto kern = sparton_fwd_kernel<CG, NP>;
+  auto kern = sparton_fwd_kernel<CG, NP, FP8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(fwd)", e);
   long long want = prm.num_units;
@@ -520,10 +537,10 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
     // Clusters must all be co-resident (static persistent schedule): a GPC
     // with an SM count not divisible by CL leaves SMs no cluster can use, and
     // any cluster beyond the resident limit would run as a serial second wave.
-    static int max_clusters[8] = {};
+    static int max_clusters[2][8] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    int& mc = max_clusters[dev & 7];
+    int& mc = max_clusters[FP8 ? 1 : 0][dev & 7];
     if (mc == 0) {
       cfg.gridDim = dim3(grid, 1, 1);
       if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
@@ -565,7 +582,7 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   const int nclusters = max(1, num_sms / cluster_ctas);
   // E group of ~48 MB stays L2-resident while H streams (see UnitIter);
   // 48 MB measured lower DRAM traffic than 4-32 MB (profiles/r01_fwd_l2_policy.txt).
-  const long long tile_bytes = (long long)tile_v * prm.D * 2;
+  const long long tile_bytes = (long long)tile_v * prm.D * (prm.fp8 ? 1 : 2);
   long long group_bytes = 48ll << 20;
   if (const char* ev = getenv("SPARTON_FWD_GROUP_KB")) group_bytes = atoll(ev) << 10;
   int gv = (int)(group_bytes / (tile_bytes > 0 ? tile_bytes : 1));
@@ -583,9 +600,81 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   if (rot < 1) rot = 1;
   while (gcd_int(rot, nclusters) != 1) ++rot;
   prm.rot = rot % nclusters;
-  if (cluster_ctas == 4) return launch_fwd_impl<2, 2>(tmE, tmH, prm, num_sms, stream);
-  if (cluster_ctas == 2) return launch_fwd_impl<2, 1>(tmE, tmH, prm, num_sms, stream);
-  return launch_fwd_impl<1, 1>(tmE, tmH, prm, num_sms, stream);
+  if (prm.fp8) {
+    if (cluster_ctas == 2) return launch_fwd_impl<2, 1, true>(tmE, tmH, prm, num_sms, stream);
+    return launch_fwd_impl<1, 1, true>(tmE, tmH, prm, num_sms, stream);
+  }
+  if (cluster_ctas == 4) return launch_fwd_impl<2, 2, false>(tmE, tmH, prm, num_sms, stream);
+  if (cluster_ctas == 2) return launch_fwd_impl<2, 1, false>(tmE, tmH, prm, num_sms, stream);
+  return launch_fwd_impl<1, 1, false>(tmE, tmH, prm, num_sms, stream);
+}
+
+// ------------------------------------------------------------------ e4m3 quantisation
+// Per-tensor scaling for the FP8 forward: amax = max |x| (non-negative floats
+// order like their bit patterns, so an integer atomicMax is exact and
+// deterministic), then q = e4m3(x * 448 / amax) with round-to-nearest and
+// saturation.  The forward dequantises with amax_h/448 * amax_e/448.
+__global__ void __launch_bounds__(256) sparton_amax_kernel(const int4* x, long long n16, unsigned* amax_bits) {
+  float m = 0.f;
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n16; i += (long long)gridDim.x * 256) {
+    const int4 a = __ldg(&x[2 * i]), b = __ldg(&x[2 * i + 1]);
+    const uint32_t w[8] = {(uint32_t)a.x, (uint32_t)a.y, (uint32_t)a.z, (uint32_t)a.w,
+                           (uint32_t)b.x, (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      m = fmaxf(m, fabsf(__uint_as_float(w[k] << 16)));
+      m = fmaxf(m, fabsf(__uint_as_float(w[k] & 0xffff0000u)));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = wm[0];
+    for (int k = 1; k < 8; ++k) t = fmaxf(t, wm[k]);
+    atomicMax(amax_bits, __float_as_uint(t));
+  }
+}
+
+__device__ __forceinline__ uint16_t e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__global__ void __launch_bounds__(256) sparton_quant_kernel(const int4* x, long long n16, int4* q,
+                                                            const float* amax) {
+  const float a = *amax;
+  const float inv = a > 0.f ? 448.0f / a : 1.0f;
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n16; i += (long long)gridDim.x * 256) {
+    const int4 u = __ldg(&x[2 * i]), v = __ldg(&x[2 * i + 1]);
+    const uint32_t w[8] = {(uint32_t)u.x, (uint32_t)u.y, (uint32_t)u.z, (uint32_t)u.w,
+                           (uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint16_t p0 = e4m3x2(__uint_as_float(w[2 * k] << 16) * inv, __uint_as_float(w[2 * k] & 0xffff0000u) * inv);
+      const uint16_t p1 = e4m3x2(__uint_as_float(w[2 * k + 1] << 16) * inv,
+                                 __uint_as_float(w[2 * k + 1] & 0xffff0000u) * inv);
+      o[k] = (uint32_t)p0 | ((uint32_t)p1 << 16);
+    }
+    q[i] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
+  }
+}
+
+int launch_quantize_e4m3(const void* x, long long n, void* q, float* amax, cudaStream_t stream) {
+  const long long n16 = n / 16;
+  cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(float), stream);
+  if (e != cudaSuccess) return set_cuda_error("cudaMemsetAsync(amax)", e);
+  int blocks = (int)std::min<long long>((n16 + 255) / 256, 148ll * 8);
+  if (blocks < 1) blocks = 1;
+  sparton_amax_kernel<<<blocks, 256, 0, stream>>>(static_cast<const int4*>(x), n16, reinterpret_cast<unsigned*>(amax));
+  sparton_quant_kernel<<<blocks, 256, 0, stream>>>(static_cast<const int4*>(x), n16, static_cast<int4*>(q), amax);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("launch e4m3 quantisation", e);
+  return SPARTON_OK;
 }
 
 // Rows of H each CTA loads per TMA box for a cluster of `cluster_ctas` CTAs.

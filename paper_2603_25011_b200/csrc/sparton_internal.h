@@ -28,6 +28,9 @@ struct FwdParams {
   int pack;            // batch rows per 256-position chunk (S = 256/pack in {32, 64, 128}), else 1
   int urows;           // unit rows: B (pack == 1) or ceil(B / pack) batch-row groups
   int n_last;          // UMMA N of a unit's last sequence chunk (multiple of 16, <= 256)
+  int fp8;             // 1: H and E are e4m3 (kind::f8f6f4), dequantised by amax_h/448 * amax_e/448
+  const float* amax_h; // device scalars (FP8 only)
+  const float* amax_e;
 };
 
 struct BwdParams {
@@ -71,6 +74,7 @@ int set_cuda_error(const char* what, cudaError_t e);
 
 int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cluster_ctas,
                int num_sms, cudaStream_t stream);
+int launch_quantize_e4m3(const void* x, long long n, void* q, float* amax, cudaStream_t stream);
 int fwd_smem_bytes(int cluster_ctas);
 int fwd_h_box_rows(int cluster_ctas);
 // H viewed as (B*S) x D bf16 with a (64 x rows) box, no swizzle (staged dE tiles).

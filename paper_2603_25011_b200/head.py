@@ -20,6 +20,8 @@ from . import _lib
 
 __all__ = [
     "sparton_forward",
+    "sparton_forward_fp8",
+    "quantize_e4m3",
     "sparton_backward",
     "SpartonHeadFn",
     "sparton_head",
@@ -99,6 +101,57 @@ def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: 
     with torch.cuda.device(H.device):
         rc = lib.sparton_fwd(Hp.data_ptr(), Ep.data_ptr(), bias.data_ptr(), m.data_ptr(),
                              Y.data_ptr(), I.data_ptr(), B, S, Dp, V, ldY, int(cta_group), _stream_ptr())
+    _lib.check(rc)
+    return Y, I
+
+
+@torch.no_grad()
+def quantize_e4m3(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Per-tensor e4m3 quantisation on the GPU: returns (q uint8 view of e4m3
+    values shaped like x, amax float32 scalar tensor); x ~= q * amax / 448."""
+    _require_cuda("x", x)
+    if x.dtype != torch.bfloat16:
+        raise ValueError(f"x must be bfloat16, got {x.dtype}")
+    xc = x.contiguous()
+    n = xc.numel()
+    if n % 16:
+        raise ValueError("numel must be a multiple of 16")
+    q = torch.empty(xc.shape, dtype=torch.uint8, device=x.device)
+    amax = torch.empty((), dtype=torch.float32, device=x.device)
+    lib = _lib.load()
+    with torch.cuda.device(x.device):
+        rc = lib.sparton_quantize_e4m3(xc.data_ptr(), n, q.data_ptr(), amax.data_ptr(), _stream_ptr())
+    _lib.check(rc)
+    return q, amax
+
+
+@torch.no_grad()
+def sparton_forward_fp8(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor, *,
+                        E_q: tuple[torch.Tensor, torch.Tensor] | None = None, cta_group: int = 0
+                        ) -> tuple[torch.Tensor, torch.Tensor]:
+    """FP8 (e4m3) variant of the fused forward — tcgen05 kind::f8f6f4 at twice
+    the bf16 tensor rate; the paper's future-work item.
+
+    H and E (bf16) are quantised per tensor on the GPU (``E_q`` may pass a
+    cached ``quantize_e4m3(E)``).  Y/I follow the same definition as
+    ``sparton_forward`` on the dequantised operands; they are approximate
+    relative to bf16 (e4m3 keeps 3 mantissa bits)."""
+    B, S, D, V = _check_inputs(H, E, bias, mask)
+    if D % 16:
+        raise ValueError("the e4m3 forward needs D to be a multiple of 16")
+    qH, aH = quantize_e4m3(H)
+    qE, aE = E_q if E_q is not None else quantize_e4m3(E)
+    m = mask.contiguous()
+    if m.dtype == torch.bool:
+        m = m.view(torch.uint8)
+    bias = bias.contiguous()
+    Y = torch.empty((B, V), dtype=torch.float32, device=H.device)
+    I = torch.empty((B, V), dtype=torch.int32, device=H.device)
+    lib = _lib.load()
+    with torch.cuda.device(H.device):
+        rc = lib.sparton_fwd_fp8(qH.data_ptr(), qE.data_ptr(), aH.data_ptr(), aE.data_ptr(), bias.data_ptr(),
+                                 m.data_ptr(), Y.data_ptr(), I.data_ptr(), B, S, D, V, V, int(cta_group),
+                                 _stream_ptr())
     _lib.check(rc)
     return Y, I
 

@@ -22,7 +22,8 @@ def _declared():
 def test_header_declares_entry_points():
     names = _declared()
     assert names == sorted(["sparton_abi_version", "sparton_last_error", "sparton_device_sm_count",
-                            "sparton_fwd", "sparton_bwd_workspace_bytes", "sparton_bwd"])
+                            "sparton_fwd", "sparton_fwd_fp8", "sparton_quantize_e4m3",
+                            "sparton_bwd_workspace_bytes", "sparton_bwd"])
 
 
 def test_library_exports_every_declared_symbol():
@@ -101,3 +102,14 @@ def test_sm_count_query_is_safe_without_gpu():
         assert n == 0
     else:
         assert n > 0
+
+
+def test_fp8_entry_points_reject_bad_arguments_before_any_cuda_call():
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    d = ctypes.c_void_p(16)
+    # D = 8 is not a multiple of 16 (e4m3 TMA stride rule)
+    assert lib.sparton_fwd_fp8(d, d, d, d, d, d, d, d, 2, 3, 8, 5, 5, 0, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_fwd_fp8(d, d, None, d, d, d, d, d, 2, 3, 16, 5, 5, 0, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_quantize_e4m3(d, 15, d, d, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_quantize_e4m3(d, 0, d, d, None) == _lib.SPARTON_EINVAL
