@@ -65,6 +65,11 @@ def test_no_cpu_fallback():
     E = torch.zeros((5, 8), dtype=torch.bfloat16)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         sparton_forward(H, E, torch.zeros(5), torch.ones((2, 3), dtype=torch.uint8))
+    from paper_2603_25011_b200 import quantize_e4m3, sparton_forward_fp8
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        sparton_forward_fp8(H, E, torch.zeros(5), torch.ones((2, 3), dtype=torch.uint8))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        quantize_e4m3(torch.zeros(16, dtype=torch.bfloat16))
 
 
 def test_backward_shape_errors_before_device_check():
