@@ -177,12 +177,12 @@ def test_shape_mismatch_rejected(cuda_device):
         sparton_backward(H, E, Y, I, torch.zeros((2, 5), device=_dev()))
 
 
-@pytest.mark.parametrize("B,D,V", [(512, 768, 30522), (512, 768, 250002), (96, 1024, 250002)])
-def test_fullsize_slices_vs_oracle(cuda_device, B, D, V):
-    """cfg2/cfg3 (and the cfg4 hidden size D=1024) backward: dH for sampled batch
-    rows and dE/db for sampled vocab columns are reproduced exactly by the
-    oracle's separable slices."""
-    S = 512
+@pytest.mark.parametrize("B,S,D,V", [(512, 512, 768, 30522), (512, 512, 768, 250002), (96, 512, 1024, 250002),
+                                     (48, 1024, 768, 30522)])
+def test_fullsize_slices_vs_oracle(cuda_device, B, S, D, V):
+    """cfg2/cfg3 (and the cfg4 hidden size D=1024; S=1024 takes the gathered
+    dE) backward: dH for sampled batch rows and dE/db for sampled vocab
+    columns are reproduced exactly by the oracle's separable slices."""
     dev = _dev()
     gen = torch.Generator(device="cuda").manual_seed(1)
     H = torch.randn((B, S, D), generator=gen, device=dev).to(torch.bfloat16)
