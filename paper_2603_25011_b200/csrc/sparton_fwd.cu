@@ -359,43 +359,78 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       // exactly 0) competes as raw -bias / dscale.
       const float nbv = -bv / dscale;
       if (p.pack > 1) {
-        // ---- packed chunk: pack batch rows of S = 256/pack positions; each
-        // 32-column group belongs to one batch row (S is a multiple of 32).
-        const int gps = p.S >> 5;                   // groups per batch row
+        // ---- packed chunk: pack = floor(256/S) batch rows of S positions
+        // (32 <= S <= 128) occupy the first pack*S columns.
         ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), aph);
         ptx::tc_fence_after();
         const uint32_t tacc = tq + (uint32_t)(acc * C::SN);
         float cbest = -INFINITY;
         int cidx = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int seg = j / gps, jj = j - seg * gps;
+        auto finish_row = [&](int seg) {
           const int bb = b * p.pack + seg;
-          const bool brow = bb < p.B;
-          const uint32_t keep = __ballot_sync(0xffffffffu,
-                                              brow && __ldg(p.mask + (size_t)(brow ? bb : 0) * p.S + jj * 32 + lane) != 0);
-          const uint32_t zero = brow ? ~keep : 0u;
-          float r[32];
-          ptx::tmem_ld32(tacc + (uint32_t)(j * 32), r);
-          ptx::tmem_ld_wait();
-          ptx::reg_fence32(r);
+          if (bb < p.B && v < p.V) {
+            const size_t o = (size_t)bb * (size_t)p.ldY + (size_t)v;
+            p.Y[o] = log1pf(fmaxf(fmaf(cbest, dscale, bv), 0.0f));
+            p.I[o] = cidx;
+          }
+          cbest = -INFINITY;
+          cidx = 0;
+        };
+        auto reduce_masked = [&](float (&r)[32], uint32_t keep, uint32_t zero, int cbase) {
           if (keep == 0xffffffffu) {
-            reduce_group_fast(r, jj * 32, cbest, cidx);
+            reduce_group_fast(r, cbase, cbest, cidx);
           } else if ((keep | zero) != 0u) {
-            const float nb = nbv;
 #pragma unroll
             for (int c = 0; c < 32; ++c)
-              r[c] = ((keep >> c) & 1u) ? r[c] : (((zero >> c) & 1u) ? nb : -INFINITY);
-            reduce_group_fast(r, jj * 32, cbest, cidx);
+              r[c] = ((keep >> c) & 1u) ? r[c] : (((zero >> c) & 1u) ? nbv : -INFINITY);
+            reduce_group_fast(r, cbase, cbest, cidx);
           }
-          if (jj == gps - 1) {                      // batch row complete
-            if (brow && v < p.V) {
-              const size_t o = (size_t)bb * (size_t)p.ldY + (size_t)v;
-              p.Y[o] = log1pf(fmaxf(fmaf(cbest, dscale, bv), 0.0f));
-              p.I[o] = cidx;
+        };
+        if ((p.S & 31) == 0) {
+          // Each 32-column group belongs to one batch row.
+          const int gps = p.S >> 5;                 // groups per batch row
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int seg = j / gps, jj = j - seg * gps;
+            if (seg < p.pack) {
+              const int bb = b * p.pack + seg;
+              const bool brow = bb < p.B;
+              const uint32_t keep = __ballot_sync(
+                  0xffffffffu, brow && __ldg(p.mask + (size_t)(brow ? bb : 0) * p.S + jj * 32 + lane) != 0);
+              float r[32];
+              ptx::tmem_ld32(tacc + (uint32_t)(j * 32), r);
+              ptx::tmem_ld_wait();
+              ptx::reg_fence32(r);
+              reduce_masked(r, keep, brow ? ~keep : 0u, jj * 32);
+              if (jj == gps - 1) finish_row(seg);
             }
-            cbest = -INFINITY;
-            cidx = 0;
+          }
+        } else {
+          // A group may straddle two batch rows (S >= 32): reduce each part
+          // separately, finishing a row at its last column.
+          const int used = p.pack * p.S;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c0 = j * 32;
+            if (c0 < used) {
+              const int last = min(c0 + 31, used - 1);
+              const int seg_a = c0 / p.S, seg_b = last / p.S;
+              const int pcol = c0 + (int)lane;
+              const int lseg = pcol / p.S;
+              const int lb = b * p.pack + lseg;
+              const bool lvalid = pcol < used && lb < p.B;
+              const bool lm = lvalid && __ldg(p.mask + (size_t)lb * p.S + (pcol - lseg * p.S)) != 0;
+              for (int seg = seg_a; seg <= seg_b; ++seg) {
+                const uint32_t keep = __ballot_sync(0xffffffffu, lm && lseg == seg);
+                const uint32_t zero = __ballot_sync(0xffffffffu, lvalid && !lm && lseg == seg);
+                float r[32];
+                ptx::tmem_ld32(tacc + (uint32_t)c0, r);
+                ptx::tmem_ld_wait();
+                ptx::reg_fence32(r);
+                reduce_masked(r, keep, zero, c0 - seg * p.S);
+                if ((seg + 1) * p.S - 1 <= last) finish_row(seg);
+              }
+            }
           }
         }
         ptx::tc_fence_before();
@@ -564,15 +599,15 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
                int num_sms, cudaStream_t stream) {
   const int tile_v = 128 * cluster_ctas;
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
-  // Short sequences (S = 32, 64, 128): pack 256/S batch rows into one 256-column
-  // chunk so the MMA computes no padding columns (SPLADE queries).
-  prm.pack = (prm.S == 32 || prm.S == 64 || prm.S == 128) ? 256 / prm.S : 1;
+  // Short sequences (32 <= S <= 128): pack floor(256/S) batch rows into one
+  // chunk so the MMA computes (almost) no padding columns (SPLADE queries).
+  prm.pack = (prm.S >= 32 && prm.S <= 128) ? 256 / prm.S : 1;
   if (const char* ev = getenv("SPARTON_FWD_PACK")) if (ev[0] == '0') prm.pack = 1;
   prm.urows = (prm.B + prm.pack - 1) / prm.pack;
   {
     // UMMA N of the last sequence chunk: the remaining positions rounded up to
     // 16 (cta_group::2 N granularity); packed chunks are always full.
-    const int rem = prm.pack > 1 ? 256 : prm.S - ((prm.S - 1) / 256) * 256;
+    const int rem = prm.pack > 1 ? prm.pack * prm.S : prm.S - ((prm.S - 1) / 256) * 256;
     prm.n_last = cluster_ctas == 1 ? 256 : ((rem + 15) / 16) * 16;
     if (const char* ev = getenv("SPARTON_FWD_NLAST")) if (ev[0] == '0') prm.n_last = 256;
   }

@@ -223,11 +223,14 @@ def test_fullsize_rows_vs_oracle(cuda_device, V, ragged):
     assert int(I.min()) >= 0 and int(I.max()) < S
 
 
-@pytest.mark.parametrize("dims", [(3, 32, 64, 700), (9, 64, 128, 2000), (5, 128, 256, 1500), (17, 32, 768, 999)])
+@pytest.mark.parametrize("dims", [(3, 32, 64, 700), (9, 64, 128, 2000), (5, 128, 256, 1500), (17, 32, 768, 999),
+                                  (7, 33, 64, 500), (5, 48, 128, 900), (4, 96, 64, 700), (6, 100, 192, 1100),
+                                  (3, 127, 64, 400)])
 @pytest.mark.parametrize("cg", [2, 1])
 def test_packed_short_sequences_vs_oracle(cuda_device, dims, cg):
-    """S in {32, 64, 128}: 256/S batch rows share one 256-column chunk (B not a
-    multiple of the pack, ragged masks, a fully masked row, bias)."""
+    """32 <= S <= 128: floor(256/S) batch rows share one chunk (groups may
+    straddle two batch rows when S is not a multiple of 32; B not a multiple
+    of the pack, ragged masks, a fully masked row, bias)."""
     B, S, D, V = dims
     H, E, b, m = orc.seeded_inputs(B, S, D, V, 70 + S, mask_keep=0.8)
     H, E = orc.bf16_round(H), orc.bf16_round(E)
@@ -237,8 +240,9 @@ def test_packed_short_sequences_vs_oracle(cuda_device, dims, cg):
     assert_parity(H, E, b, m, Yg, Ig, Yr, Ir)
 
 
-def test_packed_equals_unpacked_bitwise(cuda_device, monkeypatch):
-    B, S, D, V = 7, 64, 192, 1300
+@pytest.mark.parametrize("S", [64, 48, 100])
+def test_packed_equals_unpacked_bitwise(cuda_device, monkeypatch, S):
+    B, D, V = 7, 192, 1300
     H, E, b, m = orc.seeded_inputs(B, S, D, V, 81, mask_keep=0.9)
     H, E = orc.bf16_round(H), orc.bf16_round(E)
     Y1, I1 = run_fwd(H, E, b, m)
