@@ -360,7 +360,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       const float nbv = -bv / dscale;
       if (p.pack > 1) {
         // ---- packed chunk: pack = floor(256/S) batch rows of S positions
-        // (32 <= S <= 128) occupy the first pack*S columns.
+        // (16 <= S <= 128) occupy the first pack*S columns.
         ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), aph);
         ptx::tc_fence_after();
         const uint32_t tacc = tq + (uint32_t)(acc * C::SN);
@@ -406,8 +406,8 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
             }
           }
         } else {
-          // A group may straddle two batch rows (S >= 32): reduce each part
-          // separately, finishing a row at its last column.
+          // A group may straddle batch rows (two for S >= 32, up to three for
+          // S >= 16): reduce each part separately, finishing a row at its last column.
           const int used = p.pack * p.S;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -599,9 +599,9 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
                int num_sms, cudaStream_t stream) {
   const int tile_v = 128 * cluster_ctas;
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
-  // Short sequences (32 <= S <= 128): pack floor(256/S) batch rows into one
+  // Short sequences (16 <= S <= 128): pack floor(256/S) batch rows into one
   // chunk so the MMA computes (almost) no padding columns (SPLADE queries).
-  prm.pack = (prm.S >= 32 && prm.S <= 128) ? 256 / prm.S : 1;
+  prm.pack = (prm.S >= 16 && prm.S <= 128) ? 256 / prm.S : 1;
   if (const char* ev = getenv("SPARTON_FWD_PACK")) if (ev[0] == '0') prm.pack = 1;
   prm.urows = (prm.B + prm.pack - 1) / prm.pack;
   {

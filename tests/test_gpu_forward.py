@@ -225,7 +225,7 @@ def test_fullsize_rows_vs_oracle(cuda_device, V, ragged):
 
 @pytest.mark.parametrize("dims", [(3, 32, 64, 700), (9, 64, 128, 2000), (5, 128, 256, 1500), (17, 32, 768, 999),
                                   (7, 33, 64, 500), (5, 48, 128, 900), (4, 96, 64, 700), (6, 100, 192, 1100),
-                                  (3, 127, 64, 400)])
+                                  (3, 127, 64, 400), (40, 16, 64, 300), (23, 20, 128, 450)])
 @pytest.mark.parametrize("cg", [2, 1])
 def test_packed_short_sequences_vs_oracle(cuda_device, dims, cg):
     """32 <= S <= 128: floor(256/S) batch rows share one chunk (groups may
@@ -240,7 +240,7 @@ def test_packed_short_sequences_vs_oracle(cuda_device, dims, cg):
     assert_parity(H, E, b, m, Yg, Ig, Yr, Ir)
 
 
-@pytest.mark.parametrize("S", [64, 48, 100])
+@pytest.mark.parametrize("S", [64, 48, 100, 16, 21])
 def test_packed_equals_unpacked_bitwise(cuda_device, monkeypatch, S):
     B, D, V = 7, 192, 1300
     H, E, b, m = orc.seeded_inputs(B, S, D, V, 81, mask_keep=0.9)
