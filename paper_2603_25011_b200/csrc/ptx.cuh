@@ -109,6 +109,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// Spin variant (no suspend-time hint): for short waits on the critical path.
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  uint32_t polls = 0;
+  while (true) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    if (done) return;
+    if (++polls == (1u << 26)) __trap();
+  }
+}
+
 // One elected lane of a converged warp (elect.sync): warp-uniform control flow
 // around single-thread tcgen05 / TMA issue keeps loop state in uniform registers.
 __device__ __forceinline__ bool elect_one() {

@@ -15,7 +15,7 @@
 //                               vocab rows x 64 columns of D with fp32 sums in
 //                               registers over the whole batch; per batch row
 //                               the H[b] slice is staged in smem (TMA multicast
-//                               over a 4-CTA cluster) and every pair reads its
+//                               over a 2-CTA cluster, 4 for S > 512) and every pair reads its
 //                               argmax row from smem.  db by a column-sum kernel.
 //   K2 sparton_bwd_de_kernel  : (S > 856) CTA owns 2*W vocab rows x one D slice; warps own
 //                               2 vocab rows, lanes 8-wide D chunks; for each
@@ -331,12 +331,16 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
 // (s, g) records; every (b, v) pair then reads its argmax row from shared
 // memory.  Eight lanes own one vocab row (16 B = 8 columns each), so a warp's
 // 128-bit shared load touches four whole 128-B rows: conflict-free for any
-// argmax pattern.  The cluster's DEST_CL CTAs hold neighbouring vocab blocks
-// of the same slice: each loads S/DEST_CL rows of the tile and multicasts them
+// argmax pattern.  The cluster's CL CTAs (2 or 4) hold neighbouring vocab blocks
+// of the same slice: each loads S/CL rows of the tile and multicasts them
 // to all, so a tile costs one L2 read per cluster.  Warp NW is the TMA
 // producer; stage reuse is released cluster-wide (every consumer warp arrives
 // on the empty barrier of every CTA, since peers' multicasts write into it).
-constexpr int DEST_CL = 4;
+// Cluster size: 2 CTAs share each tile when S/2 rows fit one TMA box (S <= 512),
+// else 4.  Pairs measured 11 % faster than quads at S = 512: every stage waits
+// for the slowest consumer of the cluster before it is refilled, and the extra
+// L2 traffic of halving the multicast fan-out is cheap here.
+int de_cluster(int S) { return ((S + 1) / 2 + 7) / 8 * 8 <= 256 ? 2 : 4; }
 constexpr int DEST_DD = 64;
 
 template <int NW, int J>
@@ -356,7 +360,7 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* m, uint32_t ds
       : "memory");
 }
 
-template <int NW, int J, typename OutT>
+template <int NW, int J, int CL, typename OutT>
 __global__ void __launch_bounds__(DeStCfg<NW, J>::THREADS, 1)
 sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdParams p, int R, int nst,
                              int stage_bytes, int nvg, int nitems) {
@@ -368,12 +372,12 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
   const int lane = threadIdx.x & 31;
   const uint32_t crank = ptx::cluster_ctarank();
   // Persistent: cluster c walks work items c, c + G, ... ; item i = (vocab
-  // group i % nvg of DEST_CL blocks, D slice i / nvg).  Consecutive clusters
+  // group i % nvg of CL blocks, D slice i / nvg).  Consecutive clusters
   // share a D slice, so their H tiles are L2-shared.
-  const int cl = (int)(blockIdx.x / DEST_CL), ncl = (int)(gridDim.x / DEST_CL);
+  const int cl = (int)(blockIdx.x / CL), ncl = (int)(gridDim.x / CL);
   // Stage layout: [zero row][S-row tile][GI records].  s = -1 (inactive pair)
   // addresses the zero row, so inactive pairs never touch H.
-  const uint32_t tile_bytes = (uint32_t)(DEST_CL * R * 128);
+  const uint32_t tile_bytes = (uint32_t)(CL * R * 128);
   const uint32_t gi_off = 128 + tile_bytes;
 
   // Zero rows and GI regions start zeroed / (-1, 0): entries past the
@@ -387,7 +391,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&empty[i]), DEST_CL * NW);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), CL * NW);
     }
     ptx::fence_mbar_init();
   }
@@ -401,7 +405,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
       int st = 0;
       uint32_t ph = 0;
       for (int it = cl; it < nitems; it += ncl) {
-      const int v0 = ((it % nvg) * DEST_CL + (int)crank) * C::VB;
+      const int v0 = ((it % nvg) * CL + (int)crank) * C::VB;
       const int d0 = (it / nvg) * DEST_DD;
       const long long vrem = (long long)p.ldGI - v0;          // even
       const uint32_t gi_bytes = (uint32_t)(vrem >= C::VB ? C::GI_BYTES : (vrem > 0 ? vrem * 8 : 0));
@@ -411,7 +415,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
         const uint32_t fb = ptx::smem_u32(&full[st]);
         ptx::mbar_arrive_expect_tx(fb, tile_bytes + gi_bytes);
         tma_load_2d_mc(&tmH, sbase + 128 + crank * (uint32_t)(R * 128), fb, d0, b * p.S + (int)crank * R,
-                       (uint16_t)((1u << DEST_CL) - 1u), pol);
+                       (uint16_t)((1u << CL) - 1u), pol);
         if (gi_bytes) bulk_g2s(sbase + gi_off, p.gi + (size_t)b * p.ldGI + v0, gi_bytes, fb);
         if (++st == nst) { st = 0; ph ^= 1; }
       }
@@ -425,7 +429,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
     int st = 0;
     uint32_t ph = 0;
     for (int it = cl; it < nitems; it += ncl) {
-    const int v0 = ((it % nvg) * DEST_CL + (int)crank) * C::VB;
+    const int v0 = ((it % nvg) * CL + (int)crank) * C::VB;
     const int d0 = (it / nvg) * DEST_DD;
     float acc[J][8];
 #pragma unroll
@@ -448,7 +452,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
       // relaxed arrival (no MEMBAR) suffices to release the stage to the
       // peers' TMA writes.
       __syncwarp();
-      if (lane < DEST_CL) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&empty[st]), (uint32_t)lane));
+      if (lane < CL) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&empty[st]), (uint32_t)lane));
       if (++st == nst) { st = 0; ph ^= 1; }
     }
     const int d = d0 + sub * 8;
@@ -902,25 +906,25 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
 constexpr int DEST_SMEM_BUDGET = 227 * 1024;
 
 template <int NW, int J>
-int de_stage_bytes_t(int R) {
-  return (128 + DEST_CL * R * 128 + DeStCfg<NW, J>::GI_BYTES + 127) & ~127;
+int de_stage_bytes_t(int CL, int R) {
+  return (128 + CL * R * 128 + DeStCfg<NW, J>::GI_BYTES + 127) & ~127;
 }
 constexpr int DEST_NW = 15, DEST_J = 12;   // 720 vocab rows x 64 columns per CTA (128 regs)
-int de_stage_bytes(int R) { return de_stage_bytes_t<DEST_NW, DEST_J>(R); }
+int de_stage_bytes(int CL, int R) { return de_stage_bytes_t<DEST_NW, DEST_J>(CL, R); }
 
-template <int NW, int J, typename OutT>
+template <int NW, int J, int CL, typename OutT>
 int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
   using C = DeStCfg<NW, J>;
   const int R = de_staged_rows(p.S);
-  const int stage_bytes = de_stage_bytes_t<NW, J>(R);
+  const int stage_bytes = de_stage_bytes_t<NW, J>(CL, R);
   int nst = (DEST_SMEM_BUDGET - 128) / stage_bytes;
   if (nst > 4) nst = 4;
   const int smem = nst * stage_bytes + nst * 16;
-  auto kern = sparton_bwd_de_staged_kernel<NW, J, OutT>;
+  auto kern = sparton_bwd_de_staged_kernel<NW, J, CL, OutT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de_staged)", e);
   const int nvb = (p.V + C::VB - 1) / C::VB;
-  const int nvg = (nvb + DEST_CL - 1) / DEST_CL;
+  const int nvg = (nvb + CL - 1) / CL;
   const int nitems = nvg * ((p.D + DEST_DD - 1) / DEST_DD);
   int ncl = nitems;
   if (const char* ev = getenv("SPARTON_DE_CLUSTERS")) {   // persistent grid (SM partition experiments)
@@ -928,13 +932,13 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
     if (n > 0 && n < ncl) ncl = n;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(ncl * DEST_CL), 1, 1);
+  cfg.gridDim = dim3((unsigned)(ncl * CL), 1, 1);
   cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = DEST_CL;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -952,7 +956,8 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
 // 128 registers measured 7% faster than 11 x 17 at 168.
 template <typename OutT>
 int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
-  return launch_de_staged_t<DEST_NW, DEST_J, OutT>(p, tmH, stream);
+  if (de_cluster(p.S) == 2) return launch_de_staged_t<DEST_NW, DEST_J, 2, OutT>(p, tmH, stream);
+  return launch_de_staged_t<DEST_NW, DEST_J, 4, OutT>(p, tmH, stream);
 }
 
 template <int CPL, int W, typename OutT>
@@ -1020,10 +1025,11 @@ int launch_bwd_dtype(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t st
 // Rows of H each CTA of a staged-dE cluster loads per batch row (a multiple of
 // 8, <= 256 for one TMA box), or 0 when two pipeline stages do not fit.
 int de_staged_rows(int S) {
-  int R = (S + DEST_CL - 1) / DEST_CL;
+  const int CL = de_cluster(S);
+  int R = (S + CL - 1) / CL;
   R = (R + 7) & ~7;
   if (R > 256) return 0;
-  if (2 * de_stage_bytes(R) + 128 > DEST_SMEM_BUDGET) return 0;
+  if (2 * de_stage_bytes(CL, R) + 128 > DEST_SMEM_BUDGET) return 0;
   return R;
 }
 
