@@ -304,7 +304,8 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
   p.ldGI = ws.ldGI;
   CUtensorMap tmH;
   if (ws.de_staged) {
-    if ((rc = encode_bf16_2d_plain(&tmH, H, B * S, D, de_staged_rows((int)S), 64))) return rc;
+    const int rows = de_staged_rows((int)S);
+    if ((rc = encode_bf16_2d_plain(&tmH, H, B * S, D, rows > 256 ? 256 : rows, 64))) return rc;
   }
   return launch_bwd(p, ws.de_staged ? &tmH : nullptr, grad_dtype, static_cast<cudaStream_t>(stream));
 }

@@ -340,7 +340,13 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
 // else 4.  Pairs measured 11 % faster than quads at S = 512: every stage waits
 // for the slowest consumer of the cluster before it is refilled, and the extra
 // L2 traffic of halving the multicast fan-out is cheap here.
-int de_cluster(int S) { return ((S + 1) / 2 + 7) / 8 * 8 <= 256 ? 2 : 4; }
+int de_cluster(int S) {
+  if (const char* ev = getenv("SPARTON_DE_CL")) {   // experiment switch: 1, 2 or 4
+    const int c = atoi(ev);
+    if (c == 1 || c == 2 || c == 4) return c;
+  }
+  return ((S + 1) / 2 + 7) / 8 * 8 <= 256 ? 2 : 4;
+}
 constexpr int DEST_DD = 64;
 
 template <int NW, int J>
@@ -414,8 +420,10 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
         const uint32_t sbase = ptx::smem_u32(ds_smem + (size_t)st * stage_bytes);
         const uint32_t fb = ptx::smem_u32(&full[st]);
         ptx::mbar_arrive_expect_tx(fb, tile_bytes + gi_bytes);
-        tma_load_2d_mc(&tmH, sbase + 128 + crank * (uint32_t)(R * 128), fb, d0, b * p.S + (int)crank * R,
-                       (uint16_t)((1u << CL) - 1u), pol);
+        // R rows per CTA in boxes of at most 256 rows (the TMA box limit).
+        for (int r0 = 0; r0 < R; r0 += 256)
+          tma_load_2d_mc(&tmH, sbase + 128 + (crank * (uint32_t)R + (uint32_t)r0) * 128u, fb, d0,
+                         b * p.S + (int)crank * R + r0, (uint16_t)((1u << CL) - 1u), pol);
         if (gi_bytes) bulk_g2s(sbase + gi_off, p.gi + (size_t)b * p.ldGI + v0, gi_bytes, fb);
         if (++st == nst) { st = 0; ph ^= 1; }
       }
@@ -956,6 +964,7 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
 // 128 registers measured 7% faster than 11 x 17 at 168.
 template <typename OutT>
 int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
+  if (de_cluster(p.S) == 1) return launch_de_staged_t<DEST_NW, DEST_J, 1, OutT>(p, tmH, stream);
   if (de_cluster(p.S) == 2) return launch_de_staged_t<DEST_NW, DEST_J, 2, OutT>(p, tmH, stream);
   return launch_de_staged_t<DEST_NW, DEST_J, 4, OutT>(p, tmH, stream);
 }
@@ -1028,7 +1037,8 @@ int de_staged_rows(int S) {
   const int CL = de_cluster(S);
   int R = (S + CL - 1) / CL;
   R = (R + 7) & ~7;
-  if (R > 256) return 0;
+  if (R > 256) R = (R + 255) / 256 * 256;   // whole 256-row boxes
+  if (R > 1024) return 0;
   if (2 * de_stage_bytes(CL, R) + 128 > DEST_SMEM_BUDGET) return 0;
   return R;
 }
