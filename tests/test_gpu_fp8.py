@@ -29,8 +29,10 @@ def test_quantizer_matches_torch_e4m3(cuda_device):
     assert torch.equal(q, ref)
 
 
-@pytest.mark.parametrize("dims", [(2, 40, 64, 300), (3, 256, 128, 1000), (4, 512, 768, 3001), (9, 64, 256, 700)])
-def test_fp8_forward_vs_oracle_on_dequantised_inputs(cuda_device, dims):
+@pytest.mark.parametrize("dims", [(2, 40, 64, 300), (3, 256, 128, 1000), (4, 512, 768, 3001), (9, 64, 256, 700),
+                                  (3, 300, 96, 500)])
+@pytest.mark.parametrize("cg", [0, 1])
+def test_fp8_forward_vs_oracle_on_dequantised_inputs(cuda_device, dims, cg):
     from paper_2603_25011_b200 import quantize_e4m3, sparton_forward_fp8
     B, S, D, V = dims
     H, E, b, m = orc.seeded_inputs(B, S, D, V, 5 + S, mask_keep=0.85)
@@ -38,7 +40,7 @@ def test_fp8_forward_vs_oracle_on_dequantised_inputs(cuda_device, dims):
     Et = torch.from_numpy(E).cuda().to(torch.bfloat16)
     bt = torch.from_numpy(b).cuda()
     mt = torch.from_numpy(m).cuda()
-    Y, I = sparton_forward_fp8(Ht, Et, bt, mt)
+    Y, I = sparton_forward_fp8(Ht, Et, bt, mt, cta_group=cg)
     qH, aH = quantize_e4m3(Ht)
     qE, aE = quantize_e4m3(Et)
     Hd = (qH.view(torch.float8_e4m3fn).float() * (float(aH) / 448.0)).cpu().numpy()
