@@ -175,7 +175,6 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
   if (ldY < V) return set_error(SPARTON_EINVAL, "ldY must be >= V");
   if (cta_group != 0 && cta_group != 1 && cta_group != 2 && cta_group != 4)
     return set_error(SPARTON_EINVAL, "cta_group must be 0, 1, 2 or 4");
-  if (fp8 && cta_group == 4) return set_error(SPARTON_EINVAL, "the e4m3 forward supports cta_group 0, 1 or 2");
   if ((rc = check_device())) return rc;
   DevInfo d;
   device_info(d);
@@ -187,7 +186,6 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
     cg = 2;
     if (const char* ev = getenv("SPARTON_FWD_CLUSTER")) cg = atoi(ev);
     if (cg != 1 && cg != 2 && cg != 4) cg = 2;
-    if (fp8 && cg == 4) cg = 2;
   }
   if (const char* ev = getenv("SPARTON_L2_PERSIST_MB")) {
     // Experiment switch: L2 set-aside for evict_last (persisting) lines.

@@ -636,6 +636,7 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   while (gcd_int(rot, nclusters) != 1) ++rot;
   prm.rot = rot % nclusters;
   if (prm.fp8) {
+    if (cluster_ctas == 4) return launch_fwd_impl<2, 2, true>(tmE, tmH, prm, num_sms, stream);
     if (cluster_ctas == 2) return launch_fwd_impl<2, 1, true>(tmE, tmH, prm, num_sms, stream);
     return launch_fwd_impl<1, 1, true>(tmE, tmH, prm, num_sms, stream);
   }
