@@ -262,3 +262,14 @@ def test_narrow_last_chunk_equals_full_width_bitwise(cuda_device, monkeypatch, S
     monkeypatch.setenv("SPARTON_FWD_NLAST", "0")
     Y0, I0 = run_fwd(H, E, b, m)
     assert np.array_equal(Y1, Y0) and np.array_equal(I1, I0)
+
+
+def test_long_sequence_many_chunks(cuda_device):
+    """S = 4100: sixteen full 256-column chunks plus a narrow last one, with
+    the running argmax carried across chunks."""
+    B, S, D, V = 2, 4100, 64, 300
+    H, E, b, m = orc.seeded_inputs(B, S, D, V, 123, mask_keep=0.9)
+    H, E = orc.bf16_round(H), orc.bf16_round(E)
+    Yg, Ig = run_fwd(H, E, b, m)
+    Yr, Ir = orc.forward(H, E, b, m)
+    assert_parity(H, E, b, m, Yg, Ig, Yr, Ir)
