@@ -49,6 +49,7 @@ namespace {
 
 constexpr int DE_RPW = 2;       // vocab rows per warp (a CTA of W warps owns 2*W vocab rows)
 constexpr int DH_THREADS = 256;
+constexpr int DH_PERSIST_THREADS = 640;
 
 __device__ __forceinline__ float pair_grad(float y, float dy) {
   // exp(-Y) == 1/(1+rawmax) (fused.py:247-249); accurate expf, no fast-math.
@@ -690,8 +691,7 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long nrows = (long long)p.B * p.S;
-  // Grid-stride over rows (b*S + s): the grid may be smaller than the row count
-  // so dH can run persistently on part of the GPU next to the staged dE.
+  // Persistent grid-stride over rows (b*S + s): one CTA per SM.
   for (long long rowid = (long long)blockIdx.x * (THREADS / 32) + warp; rowid < nrows;
        rowid += (long long)gridDim.x * (THREADS / 32)) {
   const int b = (int)(rowid / p.S);
@@ -879,33 +879,24 @@ int launch_route(const BwdParams& p, cudaStream_t stream) {
 
 template <int CPL, typename OutT>
 int launch_dh(const BwdParams& p, cudaStream_t stream) {
+  // Persistent: one 640-thread CTA per SM (20 warps x 4 E rows in flight,
+  // 102 registers); warps stride over rows independently, so no warp slot
+  // idles behind a CTA's slowest row.  11.5 % faster than 3 x 256-thread CTAs
+  // per SM with 3 rows in flight (tools/ab_env.sh, locked clocks), and ahead
+  // of 24 x 3, 28 x 3, 32 x 2, 16 x 5/6, 20 x 5 and 12 x 8.
   const int dslices = (p.D + 256 * CPL - 1) / (256 * CPL);
-  const long long rows = (long long)p.B * p.S;
-  long long gx = (rows + DH_THREADS / 32 - 1) / (DH_THREADS / 32);
-  if (const char* ev = getenv("SPARTON_DH_CTAS")) {   // experiment switch: persistent grid size
-    const long long n = atoll(ev);
-    if (n > 0 && n < gx) gx = n;
-  }
-  dim3 grid((unsigned)gx, dslices);
-  // 3 E rows in flight per warp at 3 CTAs (24 warps) per SM measured 2.4 %
-  // faster than 2 x 4 and 4 x 2 (tools/ab_dh.sh, locked clocks); bypassing L1
-  // for the gathered rows (ld.global.nc.L1::no_allocate) was 56 % slower.
   const bool full = p.D % (256 * CPL) == 0;
-  if (const char* ev = getenv("SPARTON_DH_FAT")) {   // experiment: n persistent 1024-thread CTAs (1 per SM)
-    const int n = atoi(ev);
-    if (n > 0 && full) {
-      for (int c = 0; c < p.nchunks; ++c) {
-        sparton_bwd_dh_kernel<CPL, 2, 1, true, OutT, 1024><<<dim3(n, dslices), 1024, 0, stream>>>(p, c);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
-      }
-      return SPARTON_OK;
-    }
-  }
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return set_cuda_error("cudaDeviceGetAttribute(dh)", e);
+  const dim3 grid(sms, dslices);
   for (int c = 0; c < p.nchunks; ++c) {
-    if (full) sparton_bwd_dh_kernel<CPL, 3, 3, true, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
-    else sparton_bwd_dh_kernel<CPL, 2, 4, false, OutT><<<grid, DH_THREADS, 0, stream>>>(p, c);
-    cudaError_t e = cudaGetLastError();
+    if (full)
+      sparton_bwd_dh_kernel<CPL, 4, 1, true, OutT, DH_PERSIST_THREADS><<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
+    else
+      sparton_bwd_dh_kernel<CPL, 4, 1, false, OutT, DH_PERSIST_THREADS><<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
   }
   return SPARTON_OK;
