@@ -679,7 +679,7 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
 
 // ------------------------------------------------------------------ K3b: dH
 // Warp owns one (b, s) row (x D slice).  The vocabulary is processed in
-// L2-sized chunks of `wpc` route windows (~40 MB of E) by successive launches,
+// L2-sized chunks of `wpc` route windows (~52 MB of E) by successive launches,
 // so the E rows every resident warp gathers come from the same window of E.
 // Within a chunk the warp walks its (b, window, s) sub-lists in window order,
 // each in ascending v, so the accumulation order is exactly the reference's
@@ -1037,9 +1037,11 @@ int de_staged_rows(int S) {
 // Largest S the in-smem route supports (one segment of S counters + the window).
 int bwd_max_seq() { return (RT_SMEM_BUDGET - RT_WIN * 8 - 128) / 4; }
 
-// E chunk per dH pass: ~40 MB of bf16 rows so it stays L2-resident (126 MB L2)
-// next to the streaming pair lists and accumulators.
-constexpr long long DH_CHUNK_BYTES = 40ll << 20;
+// E chunk per dH pass: ~52 MB of bf16 rows (4 route windows at D = 768) so it
+// stays L2-resident (126 MB L2) next to the streaming pair lists and carries.
+// Per backward at cfg3: 8 x 52 MB passes 3.4 % faster than 11 x 38 MB, 7 x 63 MB
+// 2 % and 6 x 75 MB 3.5 % (tools/ab_env.sh, locked clocks).
+constexpr long long DH_CHUNK_BYTES = 52ll << 20;
 constexpr long long DE_CHUNK_BYTES = 48ll << 20;
 
 BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long long V, int grad_dtype) {
