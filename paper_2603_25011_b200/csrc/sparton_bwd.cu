@@ -494,8 +494,8 @@ sparton_bwd_db_kernel(const BwdParams p) {
 // ------------------------------------------------------------------ K3a: route
 // Grid (window, b).  The vocabulary is cut into windows of RT_WIN rows; for
 // each (b, window) the CTA performs a stable counting sort of the window's
-// active pairs by key s = I[b,v] entirely in shared memory and writes the
-// sorted (v, g) run out contiguously (coalesced), with per-(b, window, s)
+// active pairs by key s = I[b,v] (counters in shared memory) and scatters the
+// sorted (v, g) run into the window's output range, with per-(b, window, s)
 // offsets.  Stability: the window is split into `nseg` contiguous segments,
 // one per warp; per-(segment, s) counts give every warp its own cursors, and
 // equal keys inside a warp are ranked by lane order (match.any), so every
@@ -508,8 +508,7 @@ __global__ void __launch_bounds__(RT_THREADS)
 sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash) {
   extern __shared__ int4 rt_smem[];
   const int S = p.S;
-  int2* ent = reinterpret_cast<int2*>(rt_smem);       // [RT_WIN] sorted (v, g)
-  int* hist = reinterpret_cast<int*>(ent + RT_WIN);   // [nseg][S]
+  int* hist = reinterpret_cast<int*>(rt_smem);        // [nseg][S]
   int* scan_tmp = hist + nseg * S;                    // [32]
   const int w = blockIdx.x;
   const int b = blockIdx.y;
@@ -624,10 +623,13 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
     __syncthreads();
   }
   if (threadIdx.x == 0) off[S] = carry;
-  const int total = carry;
 
-  // Phase 3: stable scatter of (v, g) into shared memory.  Equal keys inside a
-  // warp are ranked by lane order (match.any); the bucket cursor then advances.
+  // Phase 3: stable scatter of (v, g) straight to the window's output run
+  // (the run's 64 KB is written completely by this CTA, so L2 merges the 8-byte
+  // stores; 4 % faster than sorting into shared memory and copying out).
+  // Equal keys inside a warp are ranked by lane order (match.any); the bucket
+  // cursor then advances.
+  int2* dst = p.pairs + (size_t)b * p.V + v0;
   if (warp < nseg) {
     const int vs = min(n, warp * seg_len), ve = min(n, (warp + 1) * seg_len);
     int* cur = hist + warp * S;
@@ -638,7 +640,7 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
         const unsigned peers = __match_any_sync(amask, k);
         const int rank = __popc(peers & ((1u << lane) - 1u));
         const int pos = cur[k] + rank;
-        ent[pos] = make_int2(v0 + v, __float_as_int(g));
+        dst[pos] = make_int2(v0 + v, __float_as_int(g));
         __syncwarp(amask);
         if (rank == 0) cur[k] += __popc(peers);
       }
@@ -672,9 +674,6 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
   }
   __syncthreads();
 
-  // Phase 4: coalesced copy-out of the sorted window.
-  int2* out = p.pairs + (size_t)b * p.V + v0;
-  for (int i = threadIdx.x; i < total; i += RT_THREADS) out[i] = ent[i];
 }
 
 // ------------------------------------------------------------------ K3b: dH
@@ -817,7 +816,7 @@ int route_nseg(int S) {
   if (nseg < 1) nseg = 1;
   return nseg;
 }
-size_t route_smem_bytes(int S, int nseg) { return (size_t)RT_WIN * 8 + ((size_t)nseg * S + 32) * 4; }
+size_t route_smem_bytes(int S, int nseg) { return ((size_t)nseg * S + 32) * 4; }
 
 template <int CPL, int W, bool FULL, typename OutT>
 int launch_de(const BwdParams& p, cudaStream_t stream) {
