@@ -502,9 +502,13 @@ sparton_bwd_db_kernel(const BwdParams p) {
 // (b, window, s) sub-list is in ascending v.
 constexpr int RT_THREADS = 512;
 constexpr int RT_WIN = 8192;
+// Three CTAs per SM (40 registers, ~100 B of the register stash spills to
+// L1-backed local memory): 30 % faster than two CTAs at 58 registers, and
+// ahead of four at 32 (tools/ab_kernels.sh, locked clocks).
+constexpr int RT_MINB = 3;
 constexpr int RT_SMEM_BUDGET = 200 * 1024;
 
-__global__ void __launch_bounds__(RT_THREADS)
+__global__ void __launch_bounds__(RT_THREADS, RT_MINB)
 sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash) {
   extern __shared__ int4 rt_smem[];
   const int S = p.S;
