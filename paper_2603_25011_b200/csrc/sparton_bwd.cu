@@ -883,7 +883,7 @@ int launch_route(const BwdParams& p, cudaStream_t stream) {
 template <int CPL, typename OutT>
 int launch_dh(const BwdParams& p, cudaStream_t stream) {
   // Persistent: one 640-thread CTA per SM (20 warps x 4 E rows in flight,
-  // 102 registers); warps stride over rows independently, so no warp slot
+  // 96 registers); warps stride over rows independently, so no warp slot
   // idles behind a CTA's slowest row.  11.5 % faster than 3 x 256-thread CTAs
   // per SM with 3 rows in flight (tools/ab_env.sh, locked clocks), and ahead
   // of 24 x 3, 28 x 3, 32 x 2, 16 x 5/6, 20 x 5 and 12 x 8.
