@@ -50,14 +50,17 @@ def flops(c):
     return 2 * c["B"] * c["S"] * c["V"] * c["D"], 4 * c["B"] * c["V"] * c["D"]
 
 
+DH_CHUNK_MB = 52   # csrc/sparton_bwd.cu DH_CHUNK_BYTES (tests/test_host.py keeps them equal)
+
+
 def launches_per_step(c, v_local):
     """Kernels the library launches per step (fwd + bwd) on one rank:
     K1 + route + staged dE + db column sum + one dH launch per L2-sized
     vocabulary chunk (csrc/sparton_bwd.cu: RT_WIN = 8192 rows per route
-    window, DH_CHUNK_BYTES = 40 MB of E per chunk)."""
+    window, DH_CHUNK_BYTES of E per chunk)."""
     D = c["D"]
     nwin = -(-v_local // 8192)
-    wpc = max(1, min(nwin, 32, (40 << 20) // (8192 * D * 2)))
+    wpc = max(1, min(nwin, 32, (DH_CHUNK_MB << 20) // (8192 * D * 2)))
     return 1 + 1 + 1 + 1 + -(-nwin // wpc)
 
 

@@ -102,3 +102,19 @@ def test_sweep_rejects_bad_axis_and_empty_values():
     with pytest.raises(ValueError):
         sweep.run_sweep((2, 3, 8, 5), "V", [])
     assert sweep.main(["--base", "1,2,3"]) == 2
+
+
+def test_bench_launch_count_matches_library_constants():
+    # bench.py's gpu_launches claim is derived from the library's dH chunking.
+    import re
+    from pathlib import Path
+
+    import bench
+
+    src = (Path(__file__).resolve().parent.parent / "paper_2603_25011_b200/csrc/sparton_bwd.cu").read_text()
+    chunk = int(re.search(r"constexpr long long DH_CHUNK_BYTES = (\d+)ll << 20;", src).group(1))
+    win = int(re.search(r"constexpr int RT_WIN = (\d+);", src).group(1))
+    assert bench.DH_CHUNK_MB == chunk and win == 8192
+    cfg3 = {"D": 768}
+    assert bench.launches_per_step(cfg3, 250002) == 4 + 8     # 31 windows, 4 per 52 MB pass
+    assert bench.launches_per_step(cfg3, 30522) == 4 + 1
