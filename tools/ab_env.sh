@@ -1,4 +1,5 @@
 #!/bin/bash
+mkdir -p gpurun_out
 # A/B environment switches at locked base clocks:
 #   tools/ab_env.sh <kernel regex> "VAR=a" "VAR=b" ...   ("-" = no switch)
 RX=$1; shift
