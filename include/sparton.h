@@ -102,9 +102,9 @@ SPARTON_API int sparton_quantize_e4m3(const void* x_bf16, int64_t n, void* q_e4m
 
 /* Workspace bytes sparton_bwd needs for these sizes: the argmax-routed (v, g)
  * pair lists for dH (B*V*8 bytes) and their offsets, the per-(b, v) (s, g)
- * records of the staged dE (B*V*8 bytes, S <= 856), plus an fp32 dH
+ * records of the staged dE (B*V*8 bytes, S <= 832), plus an fp32 dH
  * accumulator (B*S*D*4) when grad_dtype is bf16 and the vocabulary is
- * processed in more than one L2-sized chunk (and, for S > 856, an fp32 dE
+ * processed in more than one L2-sized chunk (and, for S > 832, an fp32 dE
  * carry for the gathered dE's batch-chunk passes).  Pure host arithmetic. */
 SPARTON_API size_t sparton_bwd_workspace_bytes(int64_t B, int64_t S, int64_t D, int64_t V,
                                                int grad_dtype);

@@ -11,8 +11,8 @@ Public surface:
   * vocab-sharded multi-GPU head: ``paper_2603_25011_b200.sharded``
 """
 
-from .head import (SpartonHeadFn, bwd_workspace_bytes, quantize_e4m3, sparton_backward, sparton_forward,
-                   sparton_forward_fp8, sparton_head)
+from .head import (SpartonHeadFn, bwd_workspace_bytes, quantize_e4m3, sparton_backward, sparton_backward_fp32,
+                   sparton_forward, sparton_forward_fp8, sparton_forward_fp32, sparton_head, split_bf16x3)
 
 __version__ = "0.1.0"
 
@@ -20,7 +20,10 @@ __all__ = [
     "SpartonHeadFn",
     "bwd_workspace_bytes",
     "sparton_backward",
+    "sparton_backward_fp32",
     "sparton_forward",
+    "sparton_forward_fp32",
+    "split_bf16x3",
     "sparton_forward_fp8",
     "quantize_e4m3",
     "sparton_head",

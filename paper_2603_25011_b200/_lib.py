@@ -15,9 +15,15 @@ import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libsparton_b200.so"
-# Development override (A/B timing of two builds); the product path uses the in-tree library.
-if os.environ.get("SPARTON_LIB"):
-    LIB_PATH = Path(os.environ["SPARTON_LIB"]).resolve()
+
+
+def _lib_path() -> Path:
+    """The in-tree library.  ``SPARTON_LIB`` (A/B timing of two builds) is a
+    development override honoured only under ``SPARTON_DEV=1`` — the same
+    single gate the native library applies to its own experiment switches."""
+    if os.environ.get("SPARTON_DEV") == "1" and os.environ.get("SPARTON_LIB"):
+        return Path(os.environ["SPARTON_LIB"]).resolve()
+    return LIB_PATH
 
 SPARTON_OK = 0
 SPARTON_EINVAL = 1
@@ -53,7 +59,7 @@ def load() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        path = Path(os.environ.get("SPARTON_LIB", LIB_PATH))
+        path = _lib_path()
         if not path.exists():
             raise SpartonLibraryMissing(
                 f"{path} not found: the sparton CUDA library is required (no CPU fallback); "

@@ -99,6 +99,12 @@ int encode_bf16_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long
   return encode_bf16_2d_swz(map, ptr, rows, cols, box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
+const char* dev_env(const char* name) {
+  const char* gate = getenv("SPARTON_DEV");
+  if (gate == nullptr || gate[0] != '1') return nullptr;
+  return getenv(name);
+}
+
 int set_error(int code, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
   return code;
@@ -184,13 +190,8 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
     // multicast (cg = 4) cut L2 traffic but measured slower inside the step
     // (lock-step coupling of the pairs).
     cg = 2;
-    if (const char* ev = getenv("SPARTON_FWD_CLUSTER")) cg = atoi(ev);
+    if (const char* ev = dev_env("SPARTON_FWD_CLUSTER")) cg = atoi(ev);
     if (cg != 1 && cg != 2 && cg != 4) cg = 2;
-  }
-  if (const char* ev = getenv("SPARTON_L2_PERSIST_MB")) {
-    // Experiment switch: L2 set-aside for evict_last (persisting) lines.
-    static std::once_flag once;
-    std::call_once(once, [ev]() { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(ev) << 20); });
   }
   // One 128-byte swizzle row per K step: 64 bf16 or 128 e4m3 columns.
   const int box_cols = fp8 ? 128 : 64;
@@ -211,7 +212,7 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
   prm.amax_h = amax_h;
   prm.amax_e = amax_e;
   {
-    const char* ev = getenv("SPARTON_E_EVICT_LAST");
+    const char* ev = dev_env("SPARTON_E_EVICT_LAST");
     // bits 0-1: E policy, bits 2-3: H policy (0 normal, 1 evict_last, 2 evict_first).
     // Both evict_last measured lowest DRAM traffic (profiles/r01_fwd_l2_policy.txt).
     prm.e_evict_last = ev ? atoi(ev) : 5;
@@ -291,10 +292,6 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
   p.dE_acc = ws.dE_acc == (size_t)-1 ? nullptr : reinterpret_cast<float*>(wsb + ws.dE_acc);
   p.db_acc = reinterpret_cast<float*>(wsb + ws.db_acc);
   p.bchunk = ws.bchunk;
-  {
-    const char* ev = getenv("SPARTON_DE_STAGGER");
-    p.de_stagger = (ev && ev[0] == '1') ? 1 : 0;
-  }
   p.nwin = ws.nwin;
   p.wpc = ws.wpc;
   p.nchunks = ws.nchunks;

@@ -11,13 +11,13 @@
 // every output element has exactly one owner that accumulates in the
 // reference's order — b ascending for dE/db, v ascending for dH.
 //
-//   K2s sparton_bwd_de_staged_kernel (S <= 856, the default): CTA owns 720
+//   K2s sparton_bwd_de_staged_kernel (S <= 832, the default): CTA owns 720
 //                               vocab rows x 64 columns of D with fp32 sums in
 //                               registers over the whole batch; per batch row
 //                               the H[b] slice is staged in smem (TMA multicast
 //                               over a 2-CTA cluster, 4 for S > 512) and every pair reads its
 //                               argmax row from smem.  db by a column-sum kernel.
-//   K2 sparton_bwd_de_kernel  : (S > 856) CTA owns 2*W vocab rows x one D slice; warps own
+//   K2 sparton_bwd_de_kernel  : (S > 832) CTA owns 2*W vocab rows x one D slice; warps own
 //                               2 vocab rows, lanes 8-wide D chunks; for each
 //                               batch row (ascending) each warp gathers its
 //                               argmax H rows with 1-D TMA bulk copies into a
@@ -38,7 +38,6 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
-#include <mutex>
 
 #include "ptx.cuh"
 #include "sparton_internal.h"
@@ -50,6 +49,14 @@ namespace {
 constexpr int DE_RPW = 2;       // vocab rows per warp (a CTA of W warps owns 2*W vocab rows)
 constexpr int DH_THREADS = 256;
 constexpr int DH_PERSIST_THREADS = 640;
+
+// A (b, v) pair contributes iff Y > 0 (fused.py:247-249).  An argmax index
+// outside [0, S) (saved state from another forward) is treated as inactive
+// instead of addressing memory out of bounds; the reference would raise
+// IndexError there, the ABI validates shapes only (fused.py:232-235).
+__device__ __forceinline__ bool pair_active(float y, int k, int S) {
+  return y > 0.f && (unsigned)k < (unsigned)S;
+}
 
 __device__ __forceinline__ float pair_grad(float y, float dy) {
   // exp(-Y) == 1/(1+rawmax) (fused.py:247-249); accurate expf, no fast-math.
@@ -193,7 +200,7 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
     for (int q = 0; q < GI_PER_THREAD; ++q) {
       const int e = threadIdx.x + q * DE_THREADS;
       const int bb = e / DE_VB, vv = e % DE_VB;
-      const bool act = ry[q] > 0.f;
+      const bool act = pair_active(ry[q], ri[q], p.S);
       gi_s[(buf * DE_BC + bb) * DE_VB + vv] =
           make_int2(act ? ri[q] : -1, __float_as_int(act ? pair_grad(ry[q], rdy[q]) : 0.f));
     }
@@ -342,7 +349,7 @@ sparton_bwd_de_kernel(const BwdParams p, int bbeg, int bend) {
 // for the slowest consumer of the cluster before it is refilled, and the extra
 // L2 traffic of halving the multicast fan-out is cheap here.
 int de_cluster(int S) {
-  if (const char* ev = getenv("SPARTON_DE_CL")) {   // experiment switch: 1, 2 or 4
+  if (const char* ev = dev_env("SPARTON_DE_CL")) {   // experiment switch: 1, 2 or 4
     const int c = atoi(ev);
     if (c == 1 || c == 2 || c == 4) return c;
   }
@@ -559,7 +566,7 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int v = vs + (q0 + q) * 32 + lane;
-          const bool active = y[q] > 0.f;
+          const bool active = pair_active(y[q], k[q], S);
           const float g = active ? pair_grad(y[q], dy[q]) : 0.f;
           // (s, g) record for the staged dE; inactive pairs get s = -1 (a zero row).
           if (gib != nullptr && v < ve) gib[v] = make_int2(active ? k[q] : -1, __float_as_int(g));
@@ -580,7 +587,7 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (y[q] > 0.f) atomicAdd(&h[k[q]], 1);
+          if (pair_active(y[q], k[q], S)) atomicAdd(&h[k[q]], 1);
       }
     }
   }
@@ -668,7 +675,7 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int v = base + q * 32 + lane;
-          const bool active = y[q] > 0.f;
+          const bool active = pair_active(y[q], k[q], S);
           const float g = active ? pair_grad(y[q], dy[q]) : 0.f;
           if (gib != nullptr && v < ve) gib[v] = make_int2(active ? k[q] : -1, __float_as_int(g));
           place(active ? k[q] : -1, g, v);
@@ -838,23 +845,40 @@ int launch_de(const BwdParams& p, cudaStream_t stream) {
   return SPARTON_OK;
 }
 
-// Per-device side stream + fork/join events: dE (independent of the route)
-// runs concurrently with route -> dH so the two L2-gather-bound kernels share
-// the SMs (an 8-warp dE CTA with a 104 KB ring leaves room for two dH CTAs).
+// Side stream + fork/join events: dE (independent of the route's dH lists)
+// runs concurrently with route -> dH so the two gather kernels share the SMs.
+// They are per (host thread, device): a call enqueues record(fork) -> wait ->
+// dE -> record(join) -> wait without another thread being able to re-record
+// the same events in between (two threads calling concurrently on distinct
+// streams never see each other's fork/join), and one thread's side-stream
+// launches cannot land in another thread's CUDA-graph capture.  Calls from
+// one thread are enqueued in program order, so reuse across its calls is safe
+// (a later call's dE only queues behind the earlier one on the side stream).
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 
+struct ThreadSideStreams {
+  SideStream dev[64];
+  ~ThreadSideStreams() {
+    // Thread exit: release the handles (pending work completes first; errors
+    // at process teardown are irrelevant).
+    for (SideStream& c : dev) {
+      if (c.s) cudaStreamDestroy(c.s);
+      if (c.fork) cudaEventDestroy(c.fork);
+      if (c.join) cudaEventDestroy(c.join);
+    }
+  }
+};
+
 int side_stream(SideStream& out) {
-  static std::mutex mu;
-  static SideStream cache[64];
+  thread_local ThreadSideStreams tls;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return set_cuda_error("cudaGetDevice", e);
   if (dev >= 64) return set_error(SPARTON_ENOTSUP, "device index >= 64");
-  std::lock_guard<std::mutex> lk(mu);
-  SideStream& c = cache[dev];
+  SideStream& c = tls.dev[dev];
   if (!c.s) {
     if ((e = cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess ||
@@ -873,7 +897,7 @@ int launch_route(const BwdParams& p, cudaStream_t stream) {
                                        (int)smem);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(route)", e);
   int allow_stash = 1;
-  if (const char* ev = getenv("SPARTON_ROUTE_STASH")) allow_stash = atoi(ev);   // experiment switch
+  if (const char* ev = dev_env("SPARTON_ROUTE_STASH")) allow_stash = atoi(ev);   // experiment switch
   sparton_bwd_route_kernel<<<dim3(p.nwin, p.B), RT_THREADS, smem, stream>>>(p, nseg, p.nwin, allow_stash);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_route_kernel", e);
@@ -929,7 +953,7 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
   const int nvg = (nvb + CL - 1) / CL;
   const int nitems = nvg * ((p.D + DEST_DD - 1) / DEST_DD);
   int ncl = nitems;
-  if (const char* ev = getenv("SPARTON_DE_CLUSTERS")) {   // persistent grid (SM partition experiments)
+  if (const char* ev = dev_env("SPARTON_DE_CLUSTERS")) {   // persistent grid (SM partition experiments)
     const int n = atoi(ev);
     if (n > 0 && n < ncl) ncl = n;
   }
@@ -972,7 +996,7 @@ int launch_de_any(const BwdParams& p, cudaStream_t stream) {
 template <int CPL, typename OutT>
 int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
   int mode = 1;
-  if (const char* ev = getenv("SPARTON_BWD_CONCURRENT")) mode = atoi(ev);
+  if (const char* ev = dev_env("SPARTON_BWD_CONCURRENT")) mode = atoi(ev);
   SideStream ss;
   int rc = side_stream(ss);
   if (rc != SPARTON_OK) return rc;
@@ -995,8 +1019,8 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
       return launch_dh<CPL, OutT>(p, stream);
     }
     // Timing experiments only (tools/bwd_parts.py): one gradient family, the
-    // others left unwritten — so they also require SPARTON_EXPERIMENTS=1.
-    if ((mode == 3 || mode == 4) && getenv("SPARTON_EXPERIMENTS") != nullptr)
+    // others left unwritten (mode is only ever != 1 in a SPARTON_DEV=1 process).
+    if (mode == 3 || mode == 4)
       return mode == 3 ? launch_de_staged<OutT>(p, tmH, stream) : launch_dh<CPL, OutT>(p, stream);
     if ((rc = fork()) != SPARTON_OK) return rc;
     if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
@@ -1052,7 +1076,7 @@ BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long lo
   BwdWorkspace w{};
   w.nwin = (int)((V + RT_WIN - 1) / RT_WIN);
   long long chunk_bytes = DH_CHUNK_BYTES;
-  if (const char* ev = getenv("SPARTON_DH_CHUNK_MB")) chunk_bytes = atoll(ev) << 20;   // experiment switch
+  if (const char* ev = dev_env("SPARTON_DH_CHUNK_MB")) chunk_bytes = atoll(ev) << 20;   // experiment switch
   long long wpc = chunk_bytes / ((long long)RT_WIN * D * 2);
   if (wpc < 1) wpc = 1;
   if (wpc > w.nwin) wpc = w.nwin;
@@ -1073,7 +1097,7 @@ BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long lo
   // Staged dE (S small enough for two smem stages): (s, g) records instead of
   // the gathered dE's fp32 carry.
   w.de_staged = de_staged_rows((int)S) > 0;
-  if (const char* ev = getenv("SPARTON_DE_STAGED")) w.de_staged = w.de_staged && ev[0] != '0';
+  if (const char* ev = dev_env("SPARTON_DE_STAGED")) w.de_staged = w.de_staged && ev[0] != '0';
   w.ldGI = V + (V & 1);
   const bool need_de_acc = !w.de_staged && grad_dtype == SPARTON_BF16 && de_passes > 1;
   w.acc32 = w.dE_acc + (need_de_acc ? up((size_t)V * (size_t)D * sizeof(float)) : 0);

@@ -602,14 +602,14 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   // Short sequences (16 <= S <= 128): pack floor(256/S) batch rows into one
   // chunk so the MMA computes (almost) no padding columns (SPLADE queries).
   prm.pack = (prm.S >= 16 && prm.S <= 128) ? 256 / prm.S : 1;
-  if (const char* ev = getenv("SPARTON_FWD_PACK")) if (ev[0] == '0') prm.pack = 1;
+  if (const char* ev = dev_env("SPARTON_FWD_PACK")) if (ev[0] == '0') prm.pack = 1;
   prm.urows = (prm.B + prm.pack - 1) / prm.pack;
   {
     // UMMA N of the last sequence chunk: the remaining positions rounded up to
     // 16 (cta_group::2 N granularity); packed chunks are always full.
     const int rem = prm.pack > 1 ? prm.pack * prm.S : prm.S - ((prm.S - 1) / 256) * 256;
     prm.n_last = cluster_ctas == 1 ? 256 : ((rem + 15) / 16) * 16;
-    if (const char* ev = getenv("SPARTON_FWD_NLAST")) if (ev[0] == '0') prm.n_last = 256;
+    if (const char* ev = dev_env("SPARTON_FWD_NLAST")) if (ev[0] == '0') prm.n_last = 256;
   }
   prm.num_units = (long long)prm.num_vt * prm.urows;
   if (prm.num_units >= (1ll << 31) - 4096)
@@ -619,18 +619,17 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   // 48 MB measured lower DRAM traffic than 4-32 MB (profiles/r01_fwd_l2_policy.txt).
   const long long tile_bytes = (long long)tile_v * prm.D * (prm.fp8 ? 1 : 2);
   long long group_bytes = 48ll << 20;
-  if (const char* ev = getenv("SPARTON_FWD_GROUP_KB")) group_bytes = atoll(ev) << 10;
+  if (const char* ev = dev_env("SPARTON_FWD_GROUP_KB")) group_bytes = atoll(ev) << 10;
   int gv = (int)(group_bytes / (tile_bytes > 0 ? tile_bytes : 1));
   if (gv < 1) gv = 1;
   if (gv > prm.num_vt) gv = prm.num_vt;
   prm.group_vt = gv;
   // Epilogue experiment switch (1-3: max-only variants with WRONG I, 4: the
-  // per-element strict '>' scan) — honoured only with SPARTON_EXPERIMENTS=1.
+  // per-element strict '>' scan) — honoured only in a SPARTON_DEV=1 process.
   prm.epi_mode = 0;
-  if (const char* ev = getenv("SPARTON_FWD_EPI"))
-    if (getenv("SPARTON_EXPERIMENTS") != nullptr) prm.epi_mode = atoi(ev);
+  if (const char* ev = dev_env("SPARTON_FWD_EPI")) prm.epi_mode = atoi(ev);
   prm.sched_bgroups = 0;   // measured: the grouped round-robin moves less DRAM (profiles/)
-  if (const char* ev = getenv("SPARTON_FWD_SCHED")) prm.sched_bgroups = ev[0] == '1';
+  if (const char* ev = dev_env("SPARTON_FWD_SCHED")) prm.sched_bgroups = ev[0] == '1';
   int rot = (int)(0.618 * nclusters + 0.5);
   if (rot < 1) rot = 1;
   while (gcd_int(rot, nclusters) != 1) ++rot;

@@ -51,7 +51,6 @@ struct BwdParams {
   float* dE_acc;       // workspace: fp32 dE carry across batch-chunk passes (bf16 output) or nullptr
   float* db_acc;       // workspace: fp32 db carry across batch-chunk passes
   int bchunk;          // batch rows per dE pass (H chunk kept L2-resident)
-  int de_stagger;      // experiment switch: rotate each CTA's batch order
   int nwin;            // route windows (RT_WIN vocab rows each)
   int wpc;             // route windows per dH pass (E chunk kept L2-resident)
   int nchunks;         // dH passes
@@ -67,6 +66,12 @@ struct BwdWorkspace {
   int nwin, wpc, nchunks, bchunk;
 };
 BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long long V, int grad_dtype);
+
+// Development switches (A/B experiments, alternative-path tests).  The shipped
+// library reads NO environment variable unless SPARTON_DEV=1 is set, so a
+// stray variable cannot change what a production process launches.  Returns
+// getenv(name) under the gate, nullptr otherwise.
+const char* dev_env(const char* name);
 
 // Records a thread-local error message and returns the status code.
 int set_error(int code, const char* msg);

@@ -1,225 +1,90 @@
-"""Drop-in mirror of the reference's ``fusedhead`` operator API, running on B200.
+"""Drop-in B200 plugin for the reference's ``fusedhead`` operator API.
 
-Same names, signatures, dataclasses and error behaviour as
-/root/reference/pkg/src/fusedhead (``__init__.py:27-46``): numpy arrays in,
-numpy arrays out, so the reference's callers (its bench harness
-``STRATEGY_RUNNERS`` at bench.py:98-104, its tests) can drive the GPU kernels
-unchanged.  Objects of the reference's own dataclasses are accepted too
-(duck typing on ``.dims/.H/.E/.b/.mask`` and ``.Y/.I``).
+The reference package (/root/reference/pkg/src/fusedhead, pure numpy) owns
+the API schema: ``Dims``, ``HeadInputs``, ``HeadOutput``, ``HeadGradients``,
+``SavedSparseState``, ``TileConfig``, the SplitMix64 input generator and the
+``AllocTracker``.  This module imports those from the installed reference
+(a user switching to the B200 kernel already has it; this repo installs it
+under the git-ignored ``baseline/_ref``) and re-exports them, so objects
+flow between the reference's own harness and the GPU path unchanged.  What
+it adds are the three operator entry points with the reference's signatures
+(fused.py:115-119, :160-164, :215-222), running on the sm_100a kernels, and
+the ``"b200"`` strategy runner for ``fusedhead.bench.STRATEGY_RUNNERS``
+(bench.py:98-104), so ``run_sweep`` / ``run_check`` drive the GPU.
 
-Numerics: H and E are rounded to bf16 (round-to-nearest-even) at the upload
-boundary and products accumulate in fp32 on the tensor cores; Y and the
-gradients are fp32.  Parity with the fp32 reference is therefore within the
-north-star tolerance (rtol 1e-2, atol 1e-3) and argmax-exact except at
-documented near-ties.  ``TileConfig`` is accepted and
-validated for API compatibility; the GPU tile shapes are compile-time
-constants, so vocab_tile / batch_tile / num_threads do not change results.
+Numerics (``PRECISION``):
+  * ``"fp32"`` (default, the reference's float32 contract): H and E are split
+    exactly into three bf16 parts and contracted on the same tensor-core
+    kernel with fp32 accumulation (``head.sparton_forward_fp32`` /
+    ``sparton_backward_fp32``) — fp32 accuracy, so the reference's own
+    harness (``run_check``, ``run_gradcheck``, tolerances bench.py:41-46)
+    passes with this module swapped in (``drop_in()``).
+  * ``"bf16"``: H and E rounded to bf16 (RNE) at the upload, one contraction —
+    9x less tensor work; parity within the north-star tolerance (rtol 1e-2,
+    atol 1e-3), argmax exact except at certified near-ties.
+``TileConfig`` is validated with the reference's own ``validate_for``; the GPU
+tile shapes are compile-time constants, so vocab_tile / batch_tile /
+num_threads do not change results.
+
+Memory accounting follows memtrack.py:1-9: the head-owned device buffers
+(the (Y, I) pair the kernel writes, B·V·8 bytes) are charged to the tracker
+through ``AllocTracker.allocate`` for the duration of the call, so a tracker
+cap yields the reference's ``AllocationCapExceeded`` (and hence its OOM
+sentinel rows in ``run_sweep``, bench.py:220-221); a real device OOM is
+reported the same way.  ``note_saved`` records the B·V·8 saved bytes.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass, replace
+import sys
+from pathlib import Path
 
 import numpy as np
 import torch
 
-from .head import sparton_backward, sparton_forward
+from .head import sparton_backward, sparton_backward_fp32, sparton_forward, sparton_forward_fp32
 
-MAX_ADDRESSABLE = 2**63 - 1
-_TILE_BUFFER_BUDGET = 1 << 20
 STRATEGY_NAME = "b200"
-
-_SM64_GAMMA = np.uint64(0x9E3779B97F4A7C15)
-_SM64_MIX1 = np.uint64(0xBF58476D1CE4E5B9)
-_SM64_MIX2 = np.uint64(0x94D049BB133111EB)
-
-
-# ---------------------------------------------------------------- types (tensor.py / reference.py / fused.py)
-
-@dataclass(frozen=True)
-class Dims:
-    """Problem sizes B, S, D, V (tensor.py:22-44), with the same overflow guard."""
-
-    B: int
-    S: int
-    D: int
-    V: int
-
-    def __post_init__(self):
-        for name in ("B", "S", "D", "V"):
-            value = getattr(self, name)
-            if not isinstance(value, int) or value < 1:
-                raise ValueError(f"dims.{name} must be a positive integer, got {value!r}")
-        if self.B * self.S * self.D > MAX_ADDRESSABLE or self.B * self.V > MAX_ADDRESSABLE:
-            raise OverflowError(f"dims {self} exceed the addressable size")
-
-    def with_axis(self, axis: str, value: int) -> "Dims":
-        field = {"batch": "B", "seq": "S", "vocab": "V"}.get(axis)
-        if field is None:
-            raise ValueError(f"unknown axis {axis!r}")
-        return replace(self, **{field: value})
+PRECISION = "fp32"
+_PRECISIONS = ("fp32", "bf16")
+_REF_INSTALL = Path(__file__).resolve().parent.parent / "baseline" / "_ref"
 
 
-@dataclass(frozen=True)
-class Uniform:
-    lo: float = -1.0
-    hi: float = 1.0
+def _import_reference():
+    """The reference package: an existing install, else this repo's
+    ``baseline/_ref`` (``python -m pip install --no-index --target
+    baseline/_ref <reference>/pkg``; ``__graft_entry__.build()`` does it)."""
+    try:
+        import fusedhead as ref
+    except ImportError:
+        if _REF_INSTALL.is_dir() and str(_REF_INSTALL) not in sys.path:
+            sys.path.append(str(_REF_INSTALL))
+        try:
+            import fusedhead as ref
+        except ImportError as exc:  # pragma: no cover - exercised only without an install
+            raise ImportError(
+                "the b200 drop-in plugs into the reference package `fusedhead`, which is not "
+                f"installed (looked in sys.path and {_REF_INSTALL}); install the reference's pkg/ "
+                "or run __graft_entry__.build()") from exc
+    return ref
 
 
-@dataclass(frozen=True)
-class Constant:
-    value: float = 0.0
+_ref = _import_reference()
 
-
-def splitmix64(seed: int, count: int) -> np.ndarray:
-    """Counter-based SplitMix64 stream, word i = mix(seed + (i+1)·γ) (tensor.py:58-69)."""
-    state = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
-    idx = np.arange(1, count + 1, dtype=np.uint64)
-    z = state + idx * _SM64_GAMMA
-    z = (z ^ (z >> np.uint64(30))) * _SM64_MIX1
-    z = (z ^ (z >> np.uint64(27))) * _SM64_MIX2
-    return z ^ (z >> np.uint64(31))
-
-
-def _unit_floats(seed: int, count: int) -> np.ndarray:
-    return (splitmix64(seed, count) >> np.uint64(11)).astype(np.float64) * (2.0**-53)
-
-
-def seeded_tensor(shape, seed: int, dist=Uniform()) -> np.ndarray:
-    """Deterministic float32 tensor (tensor.py:91-105): same bytes everywhere."""
-    shape = tuple(int(n) for n in shape)
-    if not shape or any(n < 1 for n in shape):
-        raise ValueError(f"shape must be nonempty with positive entries, got {shape}")
-    n = 1
-    for d in shape:
-        n *= d
-        if n > MAX_ADDRESSABLE:
-            raise OverflowError(f"shape {shape} overflows the addressable size")
-    if isinstance(dist, Constant):
-        return np.full(shape, np.float32(dist.value), dtype=np.float32)
-    if not isinstance(dist, Uniform):
-        raise TypeError(f"unsupported distribution {dist!r}")
-    if not dist.lo < dist.hi:
-        raise ValueError(f"uniform bounds must satisfy lo < hi, got {dist}")
-    vals = dist.lo + (dist.hi - dist.lo) * _unit_floats(seed, n)
-    return vals.astype(np.float32).reshape(shape)
-
-
-def seeded_mask(batch: int, seq: int, seed: int, keep: float = 1.0) -> np.ndarray:
-    """{0,1} uint8 mask, each position kept with probability ``keep`` (tensor.py:108-115)."""
-    if not 0.0 <= keep <= 1.0:
-        raise ValueError(f"keep must lie in [0, 1], got {keep}")
-    if keep >= 1.0:
-        return np.ones((batch, seq), np.uint8)
-    return (_unit_floats(seed, batch * seq) < keep).astype(np.uint8).reshape(batch, seq)
-
-
-def _require_finite(arr: np.ndarray, name: str) -> None:
-    if not np.isfinite(arr).all():
-        raise ValueError(f"{name} contains NaN or Inf")
-
-
-@dataclass
-class HeadInputs:
-    """(H, E, b, mask) quadruple with the reference's validation (reference.py:22-69)."""
-
-    dims: Dims
-    H: np.ndarray
-    E: np.ndarray
-    b: np.ndarray
-    mask: np.ndarray
-
-    def validate(self) -> None:
-        _validate_inputs(self)
-
-    @classmethod
-    def seeded(cls, dims: Dims, seed: int, *, mask: np.ndarray | None = None, mask_keep: float = 1.0,
-               dist=Uniform(-1.0, 1.0)) -> "HeadInputs":
-        if mask is None:
-            mask = seeded_mask(dims.B, dims.S, seed + 3, keep=mask_keep)
-        inputs = cls(dims=dims,
-                     H=seeded_tensor((dims.B, dims.S, dims.D), seed, dist),
-                     E=seeded_tensor((dims.V, dims.D), seed + 1, dist),
-                     b=seeded_tensor((dims.V,), seed + 2, dist),
-                     mask=np.ascontiguousarray(mask, dtype=np.uint8))
-        inputs.validate()
-        return inputs
-
-
-@dataclass
-class HeadOutput:
-    Y: np.ndarray
-    I: np.ndarray
-
-
-@dataclass
-class HeadGradients:
-    dH: np.ndarray
-    dE: np.ndarray
-    db: np.ndarray
-
-
-@dataclass
-class SavedSparseState:
-    """(Y, I): O(B·V) bytes, independent of S (fused.py:67-80)."""
-
-    Y: np.ndarray
-    I: np.ndarray
-
-    @classmethod
-    def from_output(cls, out) -> "SavedSparseState":
-        return cls(Y=out.Y, I=out.I)
-
-    @property
-    def nbytes(self) -> int:
-        return self.Y.nbytes + self.I.nbytes
-
-
-@dataclass(frozen=True)
-class TileConfig:
-    """Tiling policy (fused.py:37-64).  Validated for compatibility; the GPU
-    tiles are fixed (128·CG vocab rows x 256 positions x 64 K per stage)."""
-
-    vocab_tile: int
-    batch_tile: int
-    deterministic: bool = False
-    num_threads: int = 1
-
-    def validate_for(self, dims) -> None:
-        if not 1 <= self.vocab_tile <= dims.V:
-            raise ValueError(f"vocab_tile must lie in [1, {dims.V}], got {self.vocab_tile}")
-        if not 1 <= self.batch_tile <= dims.B:
-            raise ValueError(f"batch_tile must lie in [1, {dims.B}], got {self.batch_tile}")
-        if self.num_threads < 1:
-            raise ValueError(f"num_threads must be positive, got {self.num_threads}")
-
-    @classmethod
-    def default_for(cls, dims, *, deterministic: bool = False, num_threads: int = 1) -> "TileConfig":
-        c = min(64, dims.V)
-        bt = min(8, dims.B)
-        while bt > 1 and bt * dims.S * c * 4 > _TILE_BUFFER_BUDGET:
-            bt //= 2
-        while c > 1 and bt * dims.S * c * 4 > _TILE_BUFFER_BUDGET:
-            c //= 2
-        return cls(vocab_tile=c, batch_tile=bt, deterministic=deterministic, num_threads=num_threads)
-
-
-def _validate_inputs(inputs) -> None:
-    """reference.py:32-46, verbatim in behaviour: shapes, dtypes, finiteness, mask values."""
-    d = inputs.dims
-    if inputs.H.shape != (d.B, d.S, d.D) or inputs.H.dtype != np.float32:
-        raise ValueError(f"H must be float32 {(d.B, d.S, d.D)}, got {inputs.H.dtype} {inputs.H.shape}")
-    if inputs.E.shape != (d.V, d.D) or inputs.E.dtype != np.float32:
-        raise ValueError(f"E must be float32 {(d.V, d.D)}, got {inputs.E.dtype} {inputs.E.shape}")
-    if inputs.b.shape != (d.V,) or inputs.b.dtype != np.float32:
-        raise ValueError(f"b must be float32 {(d.V,)}, got {inputs.b.dtype} {inputs.b.shape}")
-    if inputs.mask.shape != (d.B, d.S) or inputs.mask.dtype != np.uint8:
-        raise ValueError(f"mask must be uint8 {(d.B, d.S)}, got {inputs.mask.dtype} {inputs.mask.shape}")
-    _require_finite(inputs.H, "H")
-    _require_finite(inputs.E, "E")
-    _require_finite(inputs.b, "b")
-    if not np.all((inputs.mask == 0) | (inputs.mask == 1)):
-        raise ValueError("mask values must be exactly 0 or 1")
+# The reference's schema, re-exported unchanged (__init__.py:27-46).
+Dims = _ref.Dims
+HeadInputs = _ref.HeadInputs
+HeadOutput = _ref.HeadOutput
+HeadGradients = _ref.HeadGradients
+SavedSparseState = _ref.SavedSparseState
+TileConfig = _ref.TileConfig
+AllocTracker = _ref.AllocTracker
+AllocationCapExceeded = _ref.AllocationCapExceeded
+Uniform = _ref.Uniform
+Constant = _ref.Constant
+seeded_tensor = _ref.seeded_tensor
+seeded_mask = _ref.seeded_mask
+splitmix64 = _ref.splitmix64
 
 
 # ---------------------------------------------------------------- device staging
@@ -230,44 +95,85 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _upload_bf16(x: np.ndarray, dev) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev).to(torch.bfloat16)
+def _precision() -> str:
+    if PRECISION not in _PRECISIONS:
+        raise ValueError(f"fusedhead.PRECISION must be one of {_PRECISIONS}, got {PRECISION!r}")
+    return PRECISION
+
+
+def _upload(x: np.ndarray, dev, precision: str) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+    return t if precision == "fp32" else t.to(torch.bfloat16)
+
+
+class _Charge:
+    """Charge the head-owned device bytes to the reference tracker for the
+    duration of a call (memtrack.py:43-55).  ``allocate`` with zero=False
+    returns an untouched host array, so the accounting costs no memory."""
+
+    def __init__(self, tracker, nbytes: int):
+        self.tracker = tracker
+        self.nbytes = nbytes
+        self.token = None
+
+    def __enter__(self):
+        if self.tracker is not None:
+            self.token = self.tracker.allocate((self.nbytes,), np.uint8, zero=False)
+        return self
+
+    def __exit__(self, *exc):
+        if self.token is not None:
+            self.tracker.release(self.token)
+        return False
+
+
+def _device_oom(tracker, nbytes: int, exc: BaseException) -> AllocationCapExceeded:
+    live = getattr(tracker, "current_bytes", 0) if tracker is not None else 0
+    cap = torch.cuda.mem_get_info()[1] if torch.cuda.is_available() else 0
+    err = AllocationCapExceeded(nbytes, live, cap)
+    err.__cause__ = exc
+    return err
 
 
 def _run_forward(inputs, tracker) -> HeadOutput:
     dev = _device()
     d = inputs.dims
-    H = _upload_bf16(inputs.H, dev)
-    E = _upload_bf16(inputs.E, dev)
-    b = torch.from_numpy(np.ascontiguousarray(inputs.b, dtype=np.float32)).to(dev)
-    m = torch.from_numpy(np.ascontiguousarray(inputs.mask, dtype=np.uint8)).to(dev)
-    Y, I = sparton_forward(H, E, b, m)
-    out = HeadOutput(Y=Y.cpu().numpy(), I=I.cpu().numpy())
+    nbytes = d.B * d.V * 8
+    with _Charge(tracker, nbytes):
+        try:
+            prec = _precision()
+            H = _upload(inputs.H, dev, prec)
+            E = _upload(inputs.E, dev, prec)
+            b = torch.from_numpy(np.ascontiguousarray(inputs.b, dtype=np.float32)).to(dev)
+            m = torch.from_numpy(np.ascontiguousarray(inputs.mask, dtype=np.uint8)).to(dev)
+            Y, I = (sparton_forward_fp32 if prec == "fp32" else sparton_forward)(H, E, b, m)
+            out = HeadOutput(Y=Y.cpu().numpy(), I=I.cpu().numpy())
+        except torch.OutOfMemoryError as exc:
+            raise _device_oom(tracker, nbytes, exc) from exc
     if tracker is not None:
         tracker.note_saved(out.Y.nbytes + out.I.nbytes)
-    assert out.Y.shape == (d.B, d.V)
     return out
 
 
-def forward_hybrid(inputs, cfg: TileConfig | None = None, tracker=None) -> HeadOutput:
+def forward_hybrid(inputs, cfg=None, tracker=None) -> HeadOutput:
     """Drop-in for fused.forward_hybrid (fused.py:115-157) on the B200 kernel."""
-    _validate_inputs(inputs)
+    inputs.validate()
     (cfg or TileConfig.default_for(inputs.dims)).validate_for(inputs.dims)
     return _run_forward(inputs, tracker)
 
 
-def forward_fully_fused(inputs, cfg: TileConfig | None = None, tracker=None) -> HeadOutput:
+def forward_fully_fused(inputs, cfg=None, tracker=None) -> HeadOutput:
     """Drop-in for fused.forward_fully_fused (fused.py:160-212): on B200 the
     streaming reduction and the hybrid are the same single fused kernel."""
-    _validate_inputs(inputs)
+    inputs.validate()
     (cfg or TileConfig.default_for(inputs.dims)).validate_for(inputs.dims)
     return _run_forward(inputs, tracker)
 
 
-def backward_fused(inputs, saved, dY: np.ndarray, cfg: TileConfig | None = None, *,
+def backward_fused(inputs, saved, dY: np.ndarray, cfg=None, *,
                    include_bias_grad: bool = True) -> HeadGradients:
-    """Drop-in for fused.backward_fused (fused.py:215-278): shape checks only,
-    gradients from (Y, I) alone, fp32 outputs."""
+    """Drop-in for fused.backward_fused (fused.py:215-278): shape checks only
+    (fused.py:232-245), gradients from (Y, I) alone, fp32 outputs."""
     d = inputs.dims
     (cfg or TileConfig.default_for(d)).validate_for(d)
     if inputs.H.shape != (d.B, d.S, d.D) or inputs.E.shape != (d.V, d.D):
@@ -277,25 +183,81 @@ def backward_fused(inputs, saved, dY: np.ndarray, cfg: TileConfig | None = None,
     if dY.shape != (d.B, d.V):
         raise ValueError(f"dY must have shape {(d.B, d.V)}, got {dY.shape}")
     dev = _device()
-    H = _upload_bf16(inputs.H, dev)
-    E = _upload_bf16(inputs.E, dev)
+    prec = _precision()
+    H = _upload(inputs.H, dev, prec)
+    E = _upload(inputs.E, dev, prec)
     Y = torch.from_numpy(np.ascontiguousarray(saved.Y, dtype=np.float32)).to(dev)
     I = torch.from_numpy(np.ascontiguousarray(saved.I, dtype=np.int32)).to(dev)
     g = torch.from_numpy(np.ascontiguousarray(dY, dtype=np.float32)).to(dev)
-    dH, dE, db = sparton_backward(H, E, Y, I, g, include_bias_grad=include_bias_grad)
+    bwd = sparton_backward_fp32 if prec == "fp32" else sparton_backward
+    dH, dE, db = bwd(H, E, Y, I, g, include_bias_grad=include_bias_grad)
     return HeadGradients(dH=dH.cpu().numpy(), dE=dE.cpu().numpy(), db=db.cpu().numpy())
 
 
-def run_b200(inputs, cfg: TileConfig, tracker) -> HeadOutput:
+def run_b200(inputs, cfg, tracker) -> HeadOutput:
     """Strategy runner with the reference's signature ``runner(inputs, cfg, tracker)``
     (bench.py:98-104)."""
     return forward_fully_fused(inputs, cfg, tracker)
 
 
-def register_strategy(runners: dict) -> None:
-    """Register the ``"b200"`` runner into a reference ``STRATEGY_RUNNERS`` dict.
-
-    Only the dict passed in is touched (the reference's acceptance test counts
-    exactly its four built-in strategy names, test_acceptance.py:278-283).
-    """
+def register_strategy(runners: dict | None = None) -> dict:
+    """Register the ``"b200"`` runner into a ``STRATEGY_RUNNERS`` dict — by
+    default the reference's own (``fusedhead.bench.STRATEGY_RUNNERS``), so its
+    ``run_sweep`` accepts ``strategies=["b200"]``.  ``STRATEGY_NAMES`` is left
+    alone: the reference's acceptance test counts exactly its four built-in
+    names (test_acceptance.py:278-283).  Returns the dict."""
+    if runners is None:
+        from fusedhead import bench as ref_bench
+        runners = ref_bench.STRATEGY_RUNNERS
     runners[STRATEGY_NAME] = run_b200
+    return runners
+
+
+def unregister_strategy(runners: dict | None = None) -> None:
+    if runners is None:
+        from fusedhead import bench as ref_bench
+        runners = ref_bench.STRATEGY_RUNNERS
+    runners.pop(STRATEGY_NAME, None)
+
+
+class drop_in:
+    """Swap the B200 operators into the reference's modules for the duration
+    of a ``with`` block: ``fusedhead.forward_hybrid`` / ``forward_fully_fused``
+    / ``backward_fused`` (package, ``fusedhead.fused`` and the names
+    ``fusedhead.bench`` imported) and the ``"b200"`` runner in
+    ``STRATEGY_RUNNERS`` — so the reference's unmodified ``run_check``,
+    ``run_gradcheck`` and ``run_sweep`` (bench.py:193-368) exercise the GPU.
+    ``precision`` sets ``PRECISION`` inside the block."""
+
+    _NAMES = ("forward_hybrid", "forward_fully_fused", "backward_fused")
+
+    def __init__(self, precision: str | None = None):
+        self.precision = precision
+        self._saved = []
+
+    def __enter__(self):
+        global PRECISION
+        import fusedhead as pkg
+        from fusedhead import bench as ref_bench, fused as ref_fused
+        mine = {"forward_hybrid": forward_hybrid, "forward_fully_fused": forward_fully_fused,
+                "backward_fused": backward_fused}
+        for mod in (pkg, ref_fused, ref_bench):
+            for n in self._NAMES:
+                if hasattr(mod, n):
+                    self._saved.append((mod, n, getattr(mod, n)))
+                    setattr(mod, n, mine[n])
+        self._prev_precision = PRECISION
+        if self.precision is not None:
+            PRECISION = self.precision
+        _precision()
+        register_strategy()
+        return self
+
+    def __exit__(self, *exc):
+        global PRECISION
+        for mod, n, fn in reversed(self._saved):
+            setattr(mod, n, fn)
+        self._saved.clear()
+        PRECISION = self._prev_precision
+        unregister_strategy()
+        return False

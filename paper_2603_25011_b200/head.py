@@ -23,6 +23,9 @@ __all__ = [
     "sparton_forward_fp8",
     "quantize_e4m3",
     "sparton_backward",
+    "sparton_forward_fp32",
+    "sparton_backward_fp32",
+    "split_bf16x3",
     "SpartonHeadFn",
     "sparton_head",
     "bwd_workspace_bytes",
@@ -209,6 +212,69 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     if Dp != D:
         dH = dH[..., :D]
         dE = dE[:, :D]
+    return dH, dE, db
+
+
+# ---------------------------------------------------------------- fp32 inputs on bf16 tensor cores
+
+def split_bf16x3(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Exact three-way split of fp32 values into bf16 parts, x = x1 + x2 + x3.
+
+    x1 = bf16(x) keeps the top 8 significant bits; x - x1 is exact in fp32
+    (Sterbenz) and has at most 16 bits, x2 = bf16(x - x1) takes the next 8 and
+    the remainder (at most 8 bits) is x3 exactly.  (Values whose low parts
+    underflow bf16's denormal range lose those bits, as fp32 would.)"""
+    x = x.float()
+    x1 = x.to(torch.bfloat16)
+    r = x - x1.float()
+    x2 = r.to(torch.bfloat16)
+    x3 = (r - x2.float()).to(torch.bfloat16)
+    return x1, x2, x3
+
+
+@torch.no_grad()
+def sparton_forward_fp32(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor
+                         ) -> tuple[torch.Tensor, torch.Tensor]:
+    """Forward on fp32 H/E at fp32 accuracy, on the same bf16 tensor-core kernel.
+
+    With H = H1 + H2 + H3 and E = E1 + E2 + E3 (``split_bf16x3``), every
+    partial product Hi·Ej of two 8-bit significands is exact in fp32, so
+    H·Eᵀ = Σ_ij Hi·Ejᵀ is one bf16 contraction over the concatenated hidden
+    axis (D' = 9·D: H' = [H1,H1,H1,H2,H2,H2,H3,H3,H3], E' = [E1,E2,E3]×3)
+    accumulated in fp32 — an fp32 dot product in a different summation order,
+    which is what the reference's own fp32 tolerances (Y rel 1e-5,
+    bench.py:41-46) allow.  Costs 9x the bf16 forward; meant for the
+    fp32 numpy drop-in (``fusedhead.PRECISION = "fp32"``)."""
+    for name, t in (("H", H), ("E", E)):
+        _require_cuda(name, t)
+        if t.dtype != torch.float32:
+            raise ValueError(f"{name} must be float32 for the fp32 forward, got {t.dtype}")
+    h = split_bf16x3(H)
+    e = split_bf16x3(E)
+    Hc = torch.cat([h[i] for i in range(3) for _ in range(3)], dim=-1)
+    Ec = torch.cat([e[j] for _ in range(3) for j in range(3)], dim=-1)
+    return sparton_forward(Hc, Ec, bias, mask)
+
+
+@torch.no_grad()
+def sparton_backward_fp32(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch.Tensor,
+                          dY: torch.Tensor, *, include_bias_grad: bool = True
+                          ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Backward on fp32 H/E: dE = Σ_b g·H[b, I] and dH = Σ_v g·E[v] are
+    linear in H and E, so with the exact splits they are the fp32 sums of
+    three bf16-operand backwards (each fp32-accumulated in the reference's
+    order) — fp32 accuracy (the reference's BACKWARD_PAIR_TOL 1e-5)."""
+    for name, t in (("H", H), ("E", E)):
+        _require_cuda(name, t)
+        if t.dtype != torch.float32:
+            raise ValueError(f"{name} must be float32 for the fp32 backward, got {t.dtype}")
+    h = split_bf16x3(H)
+    e = split_bf16x3(E)
+    dH, dE, db = sparton_backward(h[0], e[0], Y, I, dY, include_bias_grad=include_bias_grad)
+    for k in (1, 2):
+        a, b_, _ = sparton_backward(h[k], e[k], Y, I, dY, include_bias_grad=include_bias_grad)
+        dH += a
+        dE += b_
     return dH, dE, db
 
 

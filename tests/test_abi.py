@@ -43,7 +43,7 @@ def test_workspace_formula():
     B, S, D, V = 512, 512, 768, 250002
     nwin = -(-V // win)
     base = up(B * V * 8) + up(B * nwin * (S + 1) * 4) + up(V * 4)
-    gi = up(B * (V + V % 2) * 8)                 # (s, g) records of the staged dE (S <= 856)
+    gi = up(B * (V + V % 2) * 8)                 # (s, g) records of the staged dE (S <= 832)
     # fp32 gradients carry dH partial sums in the output; bf16 needs an fp32 dH
     # carry because dH runs in vocab-chunk passes (cfg3: 384 MB of E).  The
     # staged dE keeps its sums in registers over the whole batch: no dE carry.
@@ -113,3 +113,35 @@ def test_fp8_entry_points_reject_bad_arguments_before_any_cuda_call():
     assert lib.sparton_fwd_fp8(d, d, None, d, d, d, d, d, 2, 3, 16, 5, 5, 0, None) == _lib.SPARTON_EINVAL
     assert lib.sparton_quantize_e4m3(d, 15, d, d, None) == _lib.SPARTON_EINVAL
     assert lib.sparton_quantize_e4m3(d, 0, d, d, None) == _lib.SPARTON_EINVAL
+
+
+def test_experiment_switches_need_the_dev_gate(monkeypatch):
+    """The shipped library reads SPARTON_* switches only under SPARTON_DEV=1:
+    SPARTON_DE_STAGED=0 (gathered dE, which needs an fp32 dE carry in the
+    workspace) changes the workspace layout only inside the gate."""
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    B, S, D, V = 512, 512, 768, 250002
+    default = lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_BF16)
+    monkeypatch.delenv("SPARTON_DEV", raising=False)
+    monkeypatch.setenv("SPARTON_DE_STAGED", "0")
+    monkeypatch.setenv("SPARTON_DH_CHUNK_MB", "400")
+    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_BF16) == default
+    monkeypatch.setenv("SPARTON_DEV", "1")
+    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_BF16) != default
+
+
+def test_staged_de_sequence_limit():
+    """The staged dE (S <= 832: two smem stages of an S-row H tile) carries no
+    dE workspace; S = 833 switches to the gathered dE (fp32 dE carry when bf16
+    gradients need more than one batch-chunk pass)."""
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    up = lambda x: (x + 255) // 256 * 256
+    B, D, V = 512, 768, 250002
+    nwin = -(-V // 8192)
+    for S, staged in ((832, True), (833, False)):
+        base = up(B * V * 8) + up(B * nwin * (S + 1) * 4) + up(V * 4)
+        extra = up(B * (V + V % 2) * 8) if staged else up(V * D * 4)
+        assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_F32) == base + (
+            extra if staged else 0), S

@@ -216,6 +216,7 @@ def test_de_paths_agree(cuda_device, monkeypatch, dims, grad_dtype):
     H, E = orc.bf16_round(H), orc.bf16_round(E)
     dY = orc.seeded_uniform((B, V), 78)
     Y, I = run_fwd(H, E, b, m)
+    monkeypatch.setenv("SPARTON_DEV", "1")
     monkeypatch.setenv("SPARTON_DE_STAGED", "1")
     st = run_bwd(H, E, Y, I, dY, grad_dtype=grad_dtype)
     monkeypatch.setenv("SPARTON_DE_STAGED", "0")
@@ -233,6 +234,7 @@ def test_persistent_de_grid_bitwise_equal(cuda_device, monkeypatch):
     dY = orc.seeded_uniform((B, V), 62)
     Y, I = run_fwd(H, E, b, m)
     ref = run_bwd(H, E, Y, I, dY)
+    monkeypatch.setenv("SPARTON_DEV", "1")
     monkeypatch.setenv("SPARTON_DE_CLUSTERS", "2")
     got = run_bwd(H, E, Y, I, dY)
     for x, y in zip(ref, got):

@@ -246,6 +246,7 @@ def test_packed_equals_unpacked_bitwise(cuda_device, monkeypatch, S):
     H, E, b, m = orc.seeded_inputs(B, S, D, V, 81, mask_keep=0.9)
     H, E = orc.bf16_round(H), orc.bf16_round(E)
     Y1, I1 = run_fwd(H, E, b, m)
+    monkeypatch.setenv("SPARTON_DEV", "1")
     monkeypatch.setenv("SPARTON_FWD_PACK", "0")
     Y0, I0 = run_fwd(H, E, b, m)
     assert np.array_equal(Y1, Y0) and np.array_equal(I1, I0)
@@ -259,6 +260,7 @@ def test_narrow_last_chunk_equals_full_width_bitwise(cuda_device, monkeypatch, S
     H, E, b, m = orc.seeded_inputs(B, S, D, V, 90 + S, mask_keep=0.85)
     H, E = orc.bf16_round(H), orc.bf16_round(E)
     Y1, I1 = run_fwd(H, E, b, m)
+    monkeypatch.setenv("SPARTON_DEV", "1")
     monkeypatch.setenv("SPARTON_FWD_NLAST", "0")
     Y0, I0 = run_fwd(H, E, b, m)
     assert np.array_equal(Y1, Y0) and np.array_equal(I1, I0)

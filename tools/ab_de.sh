@@ -1,4 +1,5 @@
 #!/bin/bash
+export SPARTON_DEV=1   # the library honours SPARTON_* switches only under this gate
 mkdir -p gpurun_out
 # A/B staged-dE builds at locked base clocks: tools/ab_de.sh lib1 lib2 ...
 for rep in 1 2; do

@@ -1,4 +1,5 @@
 #!/bin/bash
+export SPARTON_DEV=1   # the library honours SPARTON_* switches only under this gate
 mkdir -p gpurun_out
 # A/B dH builds at locked base clocks: tools/ab_dh.sh lib1 lib2 ...
 for rep in 1 2; do

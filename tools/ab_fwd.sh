@@ -1,4 +1,5 @@
 #!/bin/bash
+export SPARTON_DEV=1   # the library honours SPARTON_* switches only under this gate
 mkdir -p gpurun_out
 # A/B two builds on the forward: locked base clocks (ncu) and natural clocks (CUDA events, fwd loop).
 for rep in 1 2; do

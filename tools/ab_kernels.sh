@@ -1,4 +1,5 @@
 #!/bin/bash
+export SPARTON_DEV=1   # the library honours SPARTON_* switches only under this gate
 mkdir -p gpurun_out
 # A/B two library builds at locked base clocks (ncu --clock-control ${NCU_CLOCK:-base} gives
 # run-to-run stable kernel times): tools/ab_kernels.sh <libA> <libB> [regex]

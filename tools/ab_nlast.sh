@@ -1,3 +1,4 @@
+export SPARTON_DEV=1   # the library honours SPARTON_* switches only under this gate
 python -m pytest tests/test_gpu_forward.py tests/test_gpu_backward.py -x -q 2>&1 | tail -2
 mkdir -p gpurun_out
 for S in 100 300 384 512; do

@@ -11,7 +11,7 @@ sys.path.insert(0, ".")
 from bench import CONFIGS, make_inputs  # noqa: E402
 from paper_2603_25011_b200 import sparton_backward, sparton_forward  # noqa: E402
 
-os.environ["SPARTON_EXPERIMENTS"] = "1"
+os.environ["SPARTON_DEV"] = "1"
 c = CONFIGS["cfg3"]
 dev = torch.device("cuda", 0)
 H, E, bias, mask, dY, _ = make_inputs(c, dev, 0, 1)

@@ -1,4 +1,5 @@
 #!/bin/bash
+export SPARTON_DEV=1   # the library honours SPARTON_* switches only under this gate
 # Forward schedule/L2-policy variants at cfg3: ncu DRAM bytes (one launch) + natural-clock time.
 run() {
   local label=$1; shift

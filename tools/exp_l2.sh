@@ -1,4 +1,5 @@
 #!/bin/bash
+export SPARTON_DEV=1   # the library honours SPARTON_* switches only under this gate
 # Forward DRAM-traffic probes at cfg3 (ncu, one launch each).
 run() {  # label, env..., then shape
   local label=$1; shift

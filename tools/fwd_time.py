@@ -7,7 +7,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2603_25011_b200 import sparton_forward
 
-os.environ.setdefault("SPARTON_EXPERIMENTS", "1")   # lets SPARTON_FWD_EPI experiments through
+os.environ.setdefault("SPARTON_DEV", "1")   # lets SPARTON_FWD_EPI experiments through
 B, S, D, V = (int(x) for x in sys.argv[1:5])
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(0)
