@@ -125,6 +125,19 @@ SPARTON_API int sparton_bwd(const void* H, const void* E, const float* Y, const 
                 int include_bias_grad, int grad_dtype,
                 void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * sparton_bwd plus an optional caller-owned cudaEvent_t (dh_ready_event,
+ * may be NULL) that is recorded on `stream` as soon as dH is final — before
+ * the call's dE/db work (which runs on a library side stream) has joined
+ * `stream`.  Lets a caller overlap a consumer of dH (the vocab-sharded
+ * head's dH all-reduce) with dE.  Everything else is sparton_bwd.
+ */
+SPARTON_API int sparton_bwd_ex(const void* H, const void* E, const float* Y, const int32_t* I,
+                const float* dY, void* dH, void* dE, float* db,
+                int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int64_t ldDY,
+                int include_bias_grad, int grad_dtype,
+                void* workspace, size_t workspace_bytes, void* stream, void* dh_ready_event);
+
 #ifdef __cplusplus
 }
 #endif

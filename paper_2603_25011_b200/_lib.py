@@ -42,6 +42,7 @@ EXPORTED = (
     "sparton_quantize_e4m3",
     "sparton_bwd_workspace_bytes",
     "sparton_bwd",
+    "sparton_bwd_ex",
 )
 
 _lock = threading.Lock()
@@ -86,6 +87,8 @@ def load() -> ctypes.CDLL:
         lib.sparton_bwd.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                     c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
                                     c_int, c_int, c_vp, ctypes.c_size_t, c_vp]
+        lib.sparton_bwd_ex.restype = c_int
+        lib.sparton_bwd_ex.argtypes = lib.sparton_bwd.argtypes + [c_vp]
         _lib = lib
         return lib
 

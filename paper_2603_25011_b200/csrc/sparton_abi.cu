@@ -251,6 +251,14 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
                 void* dH, void* dE, float* db, int64_t B, int64_t S, int64_t D, int64_t V,
                 int64_t ldY, int64_t ldDY, int include_bias_grad, int grad_dtype, void* workspace,
                 size_t workspace_bytes, void* stream) {
+  return sparton_bwd_ex(H, E, Y, I, dY, dH, dE, db, B, S, D, V, ldY, ldDY, include_bias_grad, grad_dtype,
+                        workspace, workspace_bytes, stream, nullptr);
+}
+
+int sparton_bwd_ex(const void* H, const void* E, const float* Y, const int32_t* I, const float* dY,
+                   void* dH, void* dE, float* db, int64_t B, int64_t S, int64_t D, int64_t V,
+                   int64_t ldY, int64_t ldDY, int include_bias_grad, int grad_dtype, void* workspace,
+                   size_t workspace_bytes, void* stream, void* dh_ready_event) {
   int rc = check_dims(B, S, D, V);
   if (rc) return rc;
   if (!H || !E || !Y || !I || !dY || !dH || !dE || !workspace)
@@ -297,6 +305,7 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
   p.nchunks = ws.nchunks;
   p.gi = ws.de_staged ? reinterpret_cast<int2*>(wsb + ws.gi) : nullptr;
   p.ldGI = ws.ldGI;
+  p.dh_ready = static_cast<cudaEvent_t>(dh_ready_event);
   CUtensorMap tmH;
   if (ws.de_staged) {
     const int rows = de_staged_rows((int)S);

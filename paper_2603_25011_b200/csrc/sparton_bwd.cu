@@ -39,6 +39,10 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "ptx.cuh"
 #include "sparton_internal.h"
 
@@ -859,16 +863,22 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 
+// Handles of exited threads are parked in a process-wide free list and
+// handed to the next thread that needs one: no CUDA call runs in a thread-exit
+// destructor (at process exit the runtime may already be torn down).
+// (Both intentionally leaked: a thread may exit after static destruction.)
+std::mutex& side_mu() { static std::mutex* m = new std::mutex; return *m; }
+std::vector<std::pair<int, SideStream>>& side_free() {
+  static auto* v = new std::vector<std::pair<int, SideStream>>;
+  return *v;
+}
+
 struct ThreadSideStreams {
   SideStream dev[64];
   ~ThreadSideStreams() {
-    // Thread exit: release the handles (pending work completes first; errors
-    // at process teardown are irrelevant).
-    for (SideStream& c : dev) {
-      if (c.s) cudaStreamDestroy(c.s);
-      if (c.fork) cudaEventDestroy(c.fork);
-      if (c.join) cudaEventDestroy(c.join);
-    }
+    std::lock_guard<std::mutex> lk(side_mu());
+    for (int d = 0; d < 64; ++d)
+      if (dev[d].s) side_free().emplace_back(d, dev[d]);
   }
 };
 
@@ -880,10 +890,24 @@ int side_stream(SideStream& out) {
   if (dev >= 64) return set_error(SPARTON_ENOTSUP, "device index >= 64");
   SideStream& c = tls.dev[dev];
   if (!c.s) {
-    if ((e = cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming)) != cudaSuccess)
-      return set_cuda_error("side stream setup", e);
+    {
+      std::lock_guard<std::mutex> lk(side_mu());
+      auto& fl = side_free();
+      for (size_t i = 0; i < fl.size(); ++i)
+        if (fl[i].first == dev) {
+          c = fl[i].second;
+          fl.erase(fl.begin() + (long)i);
+          break;
+        }
+    }
+    if (!c.s) {
+      SideStream n;
+      if ((e = cudaStreamCreateWithFlags(&n.s, cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming)) != cudaSuccess)
+        return set_cuda_error("side stream setup", e);
+      c = n;
+    }
   }
   out = c;
   return SPARTON_OK;
@@ -1006,6 +1030,13 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.s, ss.fork, 0);
     return e == cudaSuccess ? SPARTON_OK : set_cuda_error("fork side stream", e);
   };
+  // dH is complete on `stream` when launch_dh returns: a caller's event lets
+  // it start consuming dH (e.g. the sharded head's all-reduce) while dE runs.
+  auto dh_done = [&]() -> int {
+    if (p.dh_ready == nullptr) return SPARTON_OK;
+    e = cudaEventRecord(p.dh_ready, stream);
+    return e == cudaSuccess ? SPARTON_OK : set_cuda_error("record dh_ready", e);
+  };
   auto join = [&]() -> int {
     if ((e = cudaEventRecord(ss.join, ss.s)) != cudaSuccess) return set_cuda_error("record join", e);
     if ((e = cudaStreamWaitEvent(stream, ss.join, 0)) != cudaSuccess) return set_cuda_error("join side stream", e);
@@ -1016,7 +1047,8 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
     if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
     if (mode == 0) {
       if ((rc = launch_de_staged<OutT>(p, tmH, stream)) != SPARTON_OK) return rc;
-      return launch_dh<CPL, OutT>(p, stream);
+      if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+      return dh_done();
     }
     // Timing experiments only (tools/bwd_parts.py): one gradient family, the
     // others left unwritten (mode is only ever != 1 in a SPARTON_DEV=1 process).
@@ -1025,18 +1057,21 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
     if ((rc = fork()) != SPARTON_OK) return rc;
     if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
     if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+    if ((rc = dh_done()) != SPARTON_OK) return rc;
     return join();
   }
   if (mode == 0) {
     if ((rc = launch_de_any<CPL, 16, OutT>(p, stream)) != SPARTON_OK) return rc;
     if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
-    return launch_dh<CPL, OutT>(p, stream);
+    if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+    return dh_done();
   }
   if ((rc = fork()) != SPARTON_OK) return rc;
   rc = (mode == 2) ? launch_de_any<CPL, 16, OutT>(p, ss.s) : launch_de_any<CPL, 8, OutT>(p, ss.s);
   if (rc != SPARTON_OK) return rc;
   if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
   if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
+  if ((rc = dh_done()) != SPARTON_OK) return rc;
   return join();
 }
 

@@ -56,6 +56,7 @@ struct BwdParams {
   int nchunks;         // dH passes
   int2* gi;            // workspace: per-(b, v) (s, g) records, row stride ldGI (staged dE), or nullptr
   long long ldGI;      // even row stride of gi (16-B aligned rows)
+  cudaEvent_t dh_ready; // optional: recorded on the caller's stream once dH is final (before dE joins)
 };
 
 // Workspace layout for sparton_bwd (byte offsets, 256-B aligned).

@@ -117,7 +117,9 @@ class _Charge:
         self.token = None
 
     def __enter__(self):
-        if self.tracker is not None:
+        # Any object with the reference's allocate/release protocol is charged;
+        # a bare saved-bytes recorder (note_saved only) is not.
+        if self.tracker is not None and hasattr(self.tracker, "allocate"):
             self.token = self.tracker.allocate((self.nbytes,), np.uint8, zero=False)
         return self
 

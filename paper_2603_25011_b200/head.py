@@ -167,13 +167,18 @@ def bwd_workspace_bytes(B: int, S: int, D: int, V: int, grad_dtype: torch.dtype 
 @torch.no_grad()
 def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch.Tensor,
                      dY: torch.Tensor, *, include_bias_grad: bool = True,
-                     grad_dtype: torch.dtype = torch.float32
+                     grad_dtype: torch.dtype = torch.float32,
+                     dh_ready: torch.cuda.Event | None = None
                      ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """Argmax-routed backward from the saved (Y, I) only (fused.py:215-278).
 
     Returns (dH [B,S,D], dE [V,D], db [V] f32); dH/dE in ``grad_dtype``
     (float32 or bfloat16), accumulated in fp32 by single-owner kernels.
     Like the reference, only shapes are validated (fused.py:232-245).
+    ``dY`` may be a column slice of a wider row-major tensor (unit column
+    stride; its row stride is passed as ldDY, no copy).  ``dh_ready``, if
+    given, is recorded on the current stream as soon as dH is final, before
+    the dE work joins (``sparton_bwd_ex``).
     """
     for name, t in (("H", H), ("E", E), ("Y", Y), ("I", I), ("dY", dY)):
         _require_cuda(name, t)
@@ -194,7 +199,8 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     Dp = Hp.shape[2]
     Y = Y.contiguous()
     I = I.contiguous()
-    dY = dY.contiguous()
+    if dY.stride(1) != 1 or dY.stride(0) < V:
+        dY = dY.contiguous()
     dev = H.device
     dH = torch.empty((B, S, Dp), dtype=grad_dtype, device=dev)
     dE = torch.empty((V, Dp), dtype=grad_dtype, device=dev)
@@ -203,11 +209,16 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     gd = _lib.SPARTON_BF16 if grad_dtype == torch.bfloat16 else _lib.SPARTON_F32
     ws_bytes = int(lib.sparton_bwd_workspace_bytes(B, S, Dp, V, gd))
     ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+    ev = 0
+    if dh_ready is not None:
+        if dh_ready.cuda_event == 0:       # torch creates the event lazily on first record
+            dh_ready.record()
+        ev = dh_ready.cuda_event
     with torch.cuda.device(dev):
-        rc = lib.sparton_bwd(Hp.data_ptr(), Ep.data_ptr(), Y.data_ptr(), I.data_ptr(), dY.data_ptr(),
-                             dH.data_ptr(), dE.data_ptr(), db.data_ptr(), B, S, Dp, V, Y.stride(0),
-                             dY.stride(0), int(bool(include_bias_grad)), gd, ws.data_ptr(), ws_bytes,
-                             _stream_ptr())
+        rc = lib.sparton_bwd_ex(Hp.data_ptr(), Ep.data_ptr(), Y.data_ptr(), I.data_ptr(), dY.data_ptr(),
+                                dH.data_ptr(), dE.data_ptr(), db.data_ptr(), B, S, Dp, V, Y.stride(0),
+                                dY.stride(0), int(bool(include_bias_grad)), gd, ws.data_ptr(), ws_bytes,
+                                _stream_ptr(), ev)
     _lib.check(rc)
     if Dp != D:
         dH = dH[..., :D]

@@ -68,17 +68,47 @@ def gather_vocab(Y_p: torch.Tensor, I_p: torch.Tensor, V: int, Vp: int, group=No
 
 def local_backward(H, E_shard, Y_p, I_p, dY_p, *, grad_dtype=torch.float32, include_bias_grad=True,
                    group=None, local_bwd: Callable | None = None):
-    """Shard-local K2/K3 then an all-reduce of the partial dH (fp32)."""
-    fn = local_bwd or sparton_backward
-    dH, dE, db = fn(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
-                    grad_dtype=torch.float32)
+    """Shard-local K2/K3, then the all-reduce of the partial dH (fp32).
+
+    ``dY_p`` may be the column slice ``dY[:, v0:v1]`` of the replicated dY
+    (passed with its row stride, no copy).  On CUDA with the library's
+    backward, the all-reduce runs on its own stream as soon as dH is final
+    (``dh_ready`` event) and overlaps the shard's dE, which the library runs
+    on a side stream; the caller's stream waits for both.  The reduction is
+    in fp32 (the reference accumulates in fp32), then cast to ``grad_dtype``."""
     world, _ = _world(group)
-    if world > 1:
-        dist.all_reduce(dH, op=dist.ReduceOp.SUM, group=group)
+    if local_bwd is not None or not H.is_cuda or world == 1:
+        fn = local_bwd or sparton_backward
+        dH, dE, db = fn(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
+                        grad_dtype=torch.float32)
+        if world > 1:
+            dist.all_reduce(dH, op=dist.ReduceOp.SUM, group=group)
+    else:
+        main = torch.cuda.current_stream(H.device)
+        ready = torch.cuda.Event()
+        dH, dE, db = sparton_backward(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
+                                      grad_dtype=torch.float32, dh_ready=ready)
+        comm = _comm_stream(H.device)
+        comm.wait_event(ready)
+        with torch.cuda.stream(comm):
+            dist.all_reduce(dH, op=dist.ReduceOp.SUM, group=group)
+        dH.record_stream(comm)
+        main.wait_stream(comm)
     if grad_dtype != torch.float32:
         dH = dH.to(grad_dtype)
         dE = dE.to(grad_dtype)
     return dH, dE, db
+
+
+_COMM_STREAMS: dict = {}
+
+
+def _comm_stream(device) -> torch.cuda.Stream:
+    key = torch.device(device).index
+    s = _COMM_STREAMS.get(key)
+    if s is None:
+        s = _COMM_STREAMS[key] = torch.cuda.Stream(device=device)
+    return s
 
 
 def forward_sharded(H, E_shard, bias_shard, mask, V: int, *, group=None,
@@ -117,6 +147,8 @@ class ShardedSpartonHeadFn(torch.autograd.Function):
     def backward(ctx, dY):
         H, E_shard, Y_p, I_p = ctx.saved_tensors
         v0, v1 = ctx.v
-        dH, dE, db = local_backward(H, E_shard, Y_p, I_p, dY[:, v0:v1].contiguous().float(),
-                                    grad_dtype=H.dtype, group=ctx.group)
+        dYs = dY[:, v0:v1]
+        if dYs.dtype != torch.float32:
+            dYs = dYs.float()
+        dH, dE, db = local_backward(H, E_shard, Y_p, I_p, dYs, grad_dtype=H.dtype, group=ctx.group)
         return dH, dE.to(E_shard.dtype), db, None, None, None
