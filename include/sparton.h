@@ -96,6 +96,21 @@ SPARTON_API int sparton_fwd_fp8(const void* H8, const void* E8, const float* ama
                 int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY,
                 int cta_group, void* stream);
 
+/*
+ * sparton_fwd writing every (b, v) result to ndst (1..8) destinations with
+ * one row stride ldY: Y_dst[k] / I_dst[k] are device pointers (host array of
+ * pointers) to the first column this call covers.  For a vocab-sharded head
+ * they are the peers' symmetric [B, V] buffers offset to this shard's first
+ * column (P2P-mapped over NVLink), or one NVLS multicast address — the
+ * (Y, I) all-gather is fused into the epilogue's stores.  Destinations must
+ * not overlap.  Replaces no reference function (the reference has no
+ * multi-device path); see INTEGRATION.md.
+ */
+SPARTON_API int sparton_fwd_multi(const void* H, const void* E, const float* bias, const uint8_t* mask,
+                                  int ndst, float* const* Y_dst, int32_t* const* I_dst,
+                                  int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY,
+                                  int cta_group, void* stream);
+
 /* Per-tensor e4m3 quantisation of n bf16 values (n a multiple of 16, 16-B
  * aligned): amax (device f32 scalar) = max |x|, q = e4m3(x * 448 / amax). */
 SPARTON_API int sparton_quantize_e4m3(const void* x_bf16, int64_t n, void* q_e4m3, float* amax, void* stream);

@@ -39,6 +39,7 @@ EXPORTED = (
     "sparton_device_sm_count",
     "sparton_fwd",
     "sparton_fwd_fp8",
+    "sparton_fwd_multi",
     "sparton_quantize_e4m3",
     "sparton_bwd_workspace_bytes",
     "sparton_bwd",
@@ -76,6 +77,9 @@ def load() -> ctypes.CDLL:
         lib.sparton_fwd.restype = c_int
         lib.sparton_fwd.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                     c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]
+        lib.sparton_fwd_multi.restype = c_int
+        lib.sparton_fwd_multi.argtypes = [c_vp, c_vp, c_vp, c_vp, c_int, ctypes.POINTER(c_vp),
+                                          ctypes.POINTER(c_vp), c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]
         lib.sparton_fwd_fp8.restype = c_int
         lib.sparton_fwd_fp8.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                         c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]

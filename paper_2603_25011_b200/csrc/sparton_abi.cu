@@ -170,10 +170,14 @@ static int check_device() {
 
 static int fwd_common(const void* H, const void* E, const float* amax_h, const float* amax_e, const float* bias,
                       const uint8_t* mask, float* Y, int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V,
-                      int64_t ldY, int cta_group, void* stream, bool fp8) {
+                      int64_t ldY, int cta_group, void* stream, bool fp8, int nx = 0,
+                      float* const* Yx = nullptr, int32_t* const* Ix = nullptr) {
   int rc = check_dims(B, S, D, V);
   if (rc) return rc;
   if (!H || !E || !bias || !mask || !Y || !I) return set_error(SPARTON_EINVAL, "null pointer argument");
+  if (nx < 0 || nx > kMaxFwdDst - 1) return set_error(SPARTON_EINVAL, "ndst must lie in [1, 8]");
+  for (int k = 0; k < nx; ++k)
+    if (!Yx[k] || !Ix[k]) return set_error(SPARTON_EINVAL, "null destination pointer");
   if (fp8 && (!amax_h || !amax_e)) return set_error(SPARTON_EINVAL, "null amax pointer");
   if (fp8 && D % 16 != 0)
     return set_error(SPARTON_EINVAL, "e4m3 operands need D to be a multiple of 16 (TMA 16-byte stride)");
@@ -209,6 +213,11 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
   prm.V = (int)V;
   prm.ldY = ldY;
   prm.fp8 = fp8 ? 1 : 0;
+  prm.nx = nx;
+  for (int k = 0; k < nx; ++k) {
+    prm.Yx[k] = Yx[k];
+    prm.Ix[k] = Ix[k];
+  }
   prm.amax_h = amax_h;
   prm.amax_e = amax_e;
   {
@@ -224,6 +233,15 @@ int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* 
                 int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int cta_group,
                 void* stream) {
   return fwd_common(H, E, nullptr, nullptr, bias, mask, Y, I, B, S, D, V, ldY, cta_group, stream, false);
+}
+
+int sparton_fwd_multi(const void* H, const void* E, const float* bias, const uint8_t* mask, int ndst,
+                      float* const* Y_dst, int32_t* const* I_dst, int64_t B, int64_t S, int64_t D, int64_t V,
+                      int64_t ldY, int cta_group, void* stream) {
+  if (ndst < 1 || ndst > kMaxFwdDst || !Y_dst || !I_dst)
+    return set_error(SPARTON_EINVAL, "ndst must lie in [1, 8] with non-null destination arrays");
+  return fwd_common(H, E, nullptr, nullptr, bias, mask, Y_dst[0], I_dst[0], B, S, D, V, ldY, cta_group, stream,
+                    false, ndst - 1, Y_dst + 1, I_dst + 1);
 }
 
 int sparton_fwd_fp8(const void* H8, const void* E8, const float* amax_h, const float* amax_e, const float* bias,

@@ -176,6 +176,19 @@ __device__ __forceinline__ void reduce_group_fast(const float (&r)[32], int c0, 
   }
 }
 
+// One (b, v) result: the caller's output plus any extra destinations (the
+// peers' [B, V] copies of a vocab-sharded head, written over NVLink — the
+// all-gather fused into the epilogue).  Consecutive lanes hold consecutive v,
+// so every destination sees the same coalesced 128-B row segments.
+__device__ __forceinline__ void store_yi(const FwdParams& p, size_t o, float y, int i) {
+  p.Y[o] = y;
+  p.I[o] = i;
+  for (int k = 0; k < p.nx; ++k) {
+    p.Yx[k][o] = y;
+    p.Ix[k][o] = i;
+  }
+}
+
 template <int CG, int NP, bool FP8>
 __global__ void __launch_bounds__(FwdCfg<CG, NP, FP8>::NUM_THREADS, 1)
 sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmH,
@@ -370,8 +383,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
           const int bb = b * p.pack + seg;
           if (bb < p.B && v < p.V) {
             const size_t o = (size_t)bb * (size_t)p.ldY + (size_t)v;
-            p.Y[o] = log1pf(fmaxf(fmaf(cbest, dscale, bv), 0.0f));
-            p.I[o] = cidx;
+            store_yi(p, o, log1pf(fmaxf(fmaf(cbest, dscale, bv), 0.0f)), cidx);
           }
           cbest = -INFINITY;
           cidx = 0;
@@ -527,8 +539,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
       }
       if (v < p.V) {
         const size_t o = (size_t)b * (size_t)p.ldY + (size_t)v;
-        p.Y[o] = log1pf(fmaxf(fmaf(best, dscale, bv), 0.0f));
-        p.I[o] = bidx;
+        store_yi(p, o, log1pf(fmaxf(fmaf(best, dscale, bv), 0.0f)), bidx);
       }
     }
   }

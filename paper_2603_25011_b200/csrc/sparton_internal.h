@@ -11,11 +11,19 @@
 
 namespace sparton {
 
+constexpr int kMaxFwdDst = 8;
+
 struct FwdParams {
   const float* bias;
   const uint8_t* mask;
   float* Y;
   int32_t* I;
+  // Extra destinations (sparton_fwd_multi): every (b, v) result is also stored
+  // to Yx[k] / Ix[k] (same ldY), k < nx — the peers' copies of a sharded
+  // head's [B, V] output (P2P stores), fusing the all-gather into the epilogue.
+  int nx;
+  float* Yx[kMaxFwdDst - 1];
+  int32_t* Ix[kMaxFwdDst - 1];
   int B, S, D, V;
   long long ldY;
   int num_vt;          // number of vocab tiles
