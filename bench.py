@@ -302,9 +302,11 @@ def _max_over_ranks(vals, world, dev):
     return [float(x) for x in t]
 
 
-def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None):
+def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False):
     """Warm up, then time `steps` fwd+bwd steps between barriers; returns
-    (ms per step, mean forward ms, peak bytes, head-owned peak bytes)."""
+    (ms per step, mean forward ms, peak bytes, head-owned peak bytes, inputs).
+    ``fused``: N > 1 with the (Y, I) all-gather fused into K1's epilogue
+    (sharded.FusedVocabGather) instead of NCCL all-gather + permute copy."""
     import torch
     import torch.distributed as dist
     from paper_2603_25011_b200 import sharded, sparton_backward, sparton_forward
@@ -313,19 +315,25 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None):
     H, E, bias, mask, dY, (v0, v1, Vp) = make_inputs(c, dev, rank, world)
     stream = torch.cuda.current_stream()
     fwd_ev = [] if fwd_ev is None else fwd_ev
+    fg = sharded.FusedVocabGather(c["B"], V, dev) if fused else None
 
     def step(timed=False):
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        Y, I = sparton_forward(H, E, bias, mask)
+        if fg is not None:
+            Yg, Ig = fg.forward(H, E, bias, mask, v0)
+            Y, I = Yg[:, v0:v1], Ig[:, v0:v1]
+        else:
+            Y, I = sparton_forward(H, E, bias, mask)
         if timed:
             e1.record(stream)
             fwd_ev.append((e0, e1))
         if world == 1:
             g = sparton_backward(H, E, Y, I, dY, grad_dtype=torch.bfloat16)
         else:
-            Yg, Ig = sharded.gather_vocab(Y, I, V, Vp)
+            if fg is None:
+                Yg, Ig = sharded.gather_vocab(Y, I, V, Vp)
             g = sharded.local_backward(H, E, Y, I, dY[:, v0:v1], grad_dtype=torch.bfloat16)
         return Y, I, g
 
@@ -419,6 +427,18 @@ def run_gpu_arm(args, c, cname):
         line["e2e"] = e2e
     if world == 1 and not args.no_plugin:
         line["e2e_plugin"] = run_plugin_e2e(c, dev)
+    if world > 1 and not args.no_fused_ab:
+        # A/B of the NVLink-fused (Y, I) all-gather on the
+        # same workload; the headline keeps the NCCL path.
+        try:
+            msf, fwdf, _, _, inpf = timed_steps(c, dev, rank, world, args.steps, args.warmup, fused=True)
+            del inpf
+            line["fused_gather"] = {"ms_per_step": msf, "fwd_ms": fwdf, "value": (ff + fb) / (msf * 1e-3) / 1e12,
+                                    "unit": "TFLOP/s", "note": "K1 epilogue stores into every rank's symmetric "
+                                    "[B, V] buffers (sparton_fwd_multi) instead of NCCL all-gather"}
+        except Exception as exc:
+            line["fused_gather"] = {"unavailable": repr(exc)[:300]}
+        torch.cuda.empty_cache()
     if world > 1 and not args.no_cfg4:
         c4 = CONFIGS["cfg4"]
         ms4, fwd4, peak4, _, inp4 = timed_steps(c4, dev, rank, world, args.steps, args.warmup)
@@ -577,6 +597,7 @@ def main() -> int:
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-plugin", action="store_true", help="skip the numpy drop-in e2e record")
     ap.add_argument("--no-cfg4", action="store_true", help="N>1: skip the cfg4 record")
+    ap.add_argument("--no-fused-ab", action="store_true", help="N>1: skip the fused all-gather A/B record")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":

@@ -75,12 +75,17 @@ def _check_inputs(H, E, bias, mask):
 
 @torch.no_grad()
 def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,
-                    *, cta_group: int = 0, out: tuple[torch.Tensor, torch.Tensor] | None = None
+                    *, cta_group: int = 0, out: tuple[torch.Tensor, torch.Tensor] | None = None,
+                    extra_out: tuple[tuple[int, int], ...] = ()
                     ) -> tuple[torch.Tensor, torch.Tensor]:
     """Fused head forward: returns (Y f32 [B, V], I int32 [B, V]).
 
     Y[b,v] = log1p(relu(max_s((H[b,s]·E[v] + bias[v]) · mask[b,s]))), I = first argmax.
-    The B×S×V logits are never materialised.
+    The B×S×V logits are never materialised.  ``out`` may be column views of
+    wider row-major buffers (unit column stride, Y and I sharing a row
+    stride).  ``extra_out`` lists up to 7 more (Y, I) device addresses (raw
+    pointers, same row stride as ``out``) that receive identical stores —
+    the peers' copies of a vocab-sharded head's output (``sparton_fwd_multi``).
     """
     B, S, D, V = _check_inputs(H, E, bias, mask)
     Hp = _pad_hidden(H.contiguous()).reshape(B * S, -1)
@@ -102,8 +107,16 @@ def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: 
         raise ValueError("Y and I must share a row stride with unit column stride")
     lib = _lib.load()
     with torch.cuda.device(H.device):
-        rc = lib.sparton_fwd(Hp.data_ptr(), Ep.data_ptr(), bias.data_ptr(), m.data_ptr(),
-                             Y.data_ptr(), I.data_ptr(), B, S, Dp, V, ldY, int(cta_group), _stream_ptr())
+        if extra_out:
+            import ctypes
+            n = 1 + len(extra_out)
+            ys = (ctypes.c_void_p * n)(Y.data_ptr(), *[int(y) for y, _ in extra_out])
+            is_ = (ctypes.c_void_p * n)(I.data_ptr(), *[int(i) for _, i in extra_out])
+            rc = lib.sparton_fwd_multi(Hp.data_ptr(), Ep.data_ptr(), bias.data_ptr(), m.data_ptr(), n, ys, is_,
+                                       B, S, Dp, V, ldY, int(cta_group), _stream_ptr())
+        else:
+            rc = lib.sparton_fwd(Hp.data_ptr(), Ep.data_ptr(), bias.data_ptr(), m.data_ptr(),
+                                 Y.data_ptr(), I.data_ptr(), B, S, Dp, V, ldY, int(cta_group), _stream_ptr())
     _lib.check(rc)
     return Y, I
 
@@ -175,8 +188,9 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     Returns (dH [B,S,D], dE [V,D], db [V] f32); dH/dE in ``grad_dtype``
     (float32 or bfloat16), accumulated in fp32 by single-owner kernels.
     Like the reference, only shapes are validated (fused.py:232-245).
-    ``dY`` may be a column slice of a wider row-major tensor (unit column
-    stride; its row stride is passed as ldDY, no copy).  ``dh_ready``, if
+    ``dY`` (and Y/I, sharing one row stride) may be column slices of wider
+    row-major tensors (unit column stride; row strides passed as ldDY / ldY,
+    no copy).  ``dh_ready``, if
     given, is recorded on the current stream as soon as dH is final, before
     the dE work joins (``sparton_bwd_ex``).
     """
@@ -197,8 +211,9 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     Hp = _pad_hidden(H.contiguous())
     Ep = _pad_hidden(E.contiguous())
     Dp = Hp.shape[2]
-    Y = Y.contiguous()
-    I = I.contiguous()
+    if Y.stride(1) != 1 or I.stride(1) != 1 or I.stride(0) != Y.stride(0) or Y.stride(0) < V:
+        Y = Y.contiguous()
+        I = I.contiguous()
     if dY.stride(1) != 1 or dY.stride(0) < V:
         dY = dY.contiguous()
     dev = H.device

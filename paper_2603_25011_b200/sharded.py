@@ -66,6 +66,49 @@ def gather_vocab(Y_p: torch.Tensor, I_p: torch.Tensor, V: int, Vp: int, group=No
     return Y, I
 
 
+class FusedVocabGather:
+    """The (Y, I) all-gather fused into K1's epilogue.
+
+    Every rank holds a symmetric [B, V] (Y, I) pair (``torch.distributed.
+    _symmetric_memory``, P2P-mapped across the NVLink domain): rank p's
+    forward stores each result of its shard into EVERY rank's copy at columns
+    [v0_p, v1_p) through the peers' mapped pointers (``sparton_fwd_multi``,
+    up to 8 ranks) — no NCCL all-gather, no padded [P, B, Vp] staging and no
+    permute copy, and the NVLink transfer overlaps the MMAs unit by unit.
+    A symmetric-memory barrier before the launch (peers are done reading the
+    previous contents) and after it (every shard has landed) orders the
+    exchange on the current stream.  The returned tensors are the local
+    buffers, valid until the next ``forward``."""
+
+    def __init__(self, B: int, V: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        world, rank = _world(group)
+        if world > 8:
+            raise ValueError("the fused gather addresses at most 8 ranks (sparton_fwd_multi)")
+        self.B, self.V, self.world, self.rank = B, V, world, rank
+        grp = group if group is not None else dist.group.WORLD
+        self.Y = symm_mem.empty((B, V), dtype=torch.float32, device=device)
+        self.I = symm_mem.empty((B, V), dtype=torch.int32, device=device)
+        self.hY = symm_mem.rendezvous(self.Y, grp)
+        self.hI = symm_mem.rendezvous(self.I, grp)
+
+    def peer_destinations(self, v0: int):
+        """(Y, I) addresses of column v0 in every OTHER rank's buffers."""
+        return tuple((int(self.hY.buffer_ptrs[r]) + 4 * v0, int(self.hI.buffer_ptrs[r]) + 4 * v0)
+                     for r in range(self.world) if r != self.rank)
+
+    def forward(self, H, E_shard, bias_shard, mask, v0: int):
+        v1 = v0 + E_shard.shape[0]
+        if not 0 <= v0 <= v1 <= self.V:
+            raise ValueError(f"shard columns [{v0}, {v1}) outside [0, {self.V})")
+        self.hY.barrier(channel=0)
+        if v1 > v0:
+            sparton_forward(H, E_shard, bias_shard, mask, out=(self.Y[:, v0:v1], self.I[:, v0:v1]),
+                            extra_out=self.peer_destinations(v0))
+        self.hY.barrier(channel=1)
+        return self.Y, self.I
+
+
 def local_backward(H, E_shard, Y_p, I_p, dY_p, *, grad_dtype=torch.float32, include_bias_grad=True,
                    group=None, local_bwd: Callable | None = None):
     """Shard-local K2/K3, then the all-reduce of the partial dH (fp32).

@@ -45,3 +45,5 @@ def test_bench_two_ranks_one_gpu(cuda_device):
     c4 = d["cfg4"]
     assert c4["config"]["workload"] == "cfg4" and c4["config"]["D"] == 1024 and c4["config"]["B"] == 2048
     assert c4["value"] > 0 and c4["ms_per_step"] > 0
+    fg = d["fused_gather"]
+    assert "unavailable" in fg or fg["value"] > 0
