@@ -315,7 +315,7 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False):
     H, E, bias, mask, dY, (v0, v1, Vp) = make_inputs(c, dev, rank, world)
     stream = torch.cuda.current_stream()
     fwd_ev = [] if fwd_ev is None else fwd_ev
-    fg = sharded.FusedVocabGather(c["B"], V, dev) if fused else None
+    fg = sharded.FusedVocabGather.symmetric(c["B"], V, dev) if fused else None
 
     def step(timed=False):
         if timed:

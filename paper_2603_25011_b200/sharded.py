@@ -69,43 +69,55 @@ def gather_vocab(Y_p: torch.Tensor, I_p: torch.Tensor, V: int, Vp: int, group=No
 class FusedVocabGather:
     """The (Y, I) all-gather fused into K1's epilogue.
 
-    Every rank holds a symmetric [B, V] (Y, I) pair (``torch.distributed.
-    _symmetric_memory``, P2P-mapped across the NVLink domain): rank p's
-    forward stores each result of its shard into EVERY rank's copy at columns
-    [v0_p, v1_p) through the peers' mapped pointers (``sparton_fwd_multi``,
-    up to 8 ranks) — no NCCL all-gather, no padded [P, B, Vp] staging and no
-    permute copy, and the NVLink transfer overlaps the MMAs unit by unit.
-    A symmetric-memory barrier before the launch (peers are done reading the
-    previous contents) and after it (every shard has landed) orders the
-    exchange on the current stream.  The returned tensors are the local
-    buffers, valid until the next ``forward``."""
+    Every rank holds a [B, V] (Y, I) pair that all other ranks can address:
+    rank p's forward stores each result of its shard into EVERY rank's copy at
+    columns [v0_p, v1_p) through the peers' mapped pointers
+    (``sparton_fwd_multi``, up to 8 ranks) — no NCCL all-gather, no padded
+    [P, B, Vp] staging and no permute copy, and the NVLink transfer overlaps
+    the MMAs unit by unit.  A barrier before the launch (peers are done reading
+    the previous contents) and after it (every shard has landed) orders the
+    exchange.  The returned tensors are the local buffers, valid until the
+    next ``forward``.
 
-    def __init__(self, B: int, V: int, device, group=None):
+    ``FusedVocabGather.symmetric(B, V, device, group)`` is the production
+    constructor: torch symmetric memory (P2P-mapped across the NVLink domain)
+    and its device-side barrier on the current stream.  The plain constructor
+    takes already-mapped peer buffers and a barrier callable (the one-GPU test
+    maps the peers' buffers with CUDA IPC)."""
+
+    def __init__(self, Y: torch.Tensor, I: torch.Tensor, peers, barrier: Callable[[int], None],
+                 keepalive=()):
+        if Y.shape != I.shape or Y.dtype != torch.float32 or I.dtype != torch.int32:
+            raise ValueError("Y must be float32 and I int32 of the same [B, V] shape")
+        if len(peers) > 7:
+            raise ValueError("the fused gather addresses at most 8 ranks (sparton_fwd_multi)")
+        self.Y, self.I = Y, I
+        self.B, self.V = Y.shape
+        self.peers = [(int(y), int(i)) for y, i in peers]
+        self.barrier = barrier
+        self._keepalive = keepalive
+
+    @classmethod
+    def symmetric(cls, B: int, V: int, device, group=None) -> "FusedVocabGather":
         import torch.distributed._symmetric_memory as symm_mem
         world, rank = _world(group)
-        if world > 8:
-            raise ValueError("the fused gather addresses at most 8 ranks (sparton_fwd_multi)")
-        self.B, self.V, self.world, self.rank = B, V, world, rank
         grp = group if group is not None else dist.group.WORLD
-        self.Y = symm_mem.empty((B, V), dtype=torch.float32, device=device)
-        self.I = symm_mem.empty((B, V), dtype=torch.int32, device=device)
-        self.hY = symm_mem.rendezvous(self.Y, grp)
-        self.hI = symm_mem.rendezvous(self.I, grp)
-
-    def peer_destinations(self, v0: int):
-        """(Y, I) addresses of column v0 in every OTHER rank's buffers."""
-        return tuple((int(self.hY.buffer_ptrs[r]) + 4 * v0, int(self.hI.buffer_ptrs[r]) + 4 * v0)
-                     for r in range(self.world) if r != self.rank)
+        Y = symm_mem.empty((B, V), dtype=torch.float32, device=device)
+        I = symm_mem.empty((B, V), dtype=torch.int32, device=device)
+        hY = symm_mem.rendezvous(Y, grp)
+        hI = symm_mem.rendezvous(I, grp)
+        peers = [(hY.buffer_ptrs[r], hI.buffer_ptrs[r]) for r in range(world) if r != rank]
+        return cls(Y, I, peers, lambda ch: hY.barrier(channel=ch), keepalive=(hY, hI))
 
     def forward(self, H, E_shard, bias_shard, mask, v0: int):
         v1 = v0 + E_shard.shape[0]
         if not 0 <= v0 <= v1 <= self.V:
             raise ValueError(f"shard columns [{v0}, {v1}) outside [0, {self.V})")
-        self.hY.barrier(channel=0)
+        self.barrier(0)
         if v1 > v0:
             sparton_forward(H, E_shard, bias_shard, mask, out=(self.Y[:, v0:v1], self.I[:, v0:v1]),
-                            extra_out=self.peer_destinations(v0))
-        self.hY.barrier(channel=1)
+                            extra_out=tuple((y + 4 * v0, i + 4 * v0) for y, i in self.peers))
+        self.barrier(1)
         return self.Y, self.I
 
 
