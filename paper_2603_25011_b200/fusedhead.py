@@ -20,7 +20,7 @@ Numerics (``PRECISION``):
     harness (``run_check``, ``run_gradcheck``, tolerances bench.py:41-46)
     passes with this module swapped in (``drop_in()``).
   * ``"bf16"``: H and E rounded to bf16 (RNE) at the upload, one contraction —
-    9x less tensor work; parity within the north-star tolerance (rtol 1e-2,
+    6x less tensor work; parity within the north-star tolerance (rtol 1e-2,
     atol 1e-3), argmax exact except at certified near-ties.
 ``TileConfig`` is validated with the reference's own ``validate_for``; the GPU
 tile shapes are compile-time constants, so vocab_tile / batch_tile /
