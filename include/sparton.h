@@ -153,6 +153,22 @@ SPARTON_API int sparton_bwd_ex(const void* H, const void* E, const float* Y, con
                 int include_bias_grad, int grad_dtype,
                 void* workspace, size_t workspace_bytes, void* stream, void* dh_ready_event);
 
+/*
+ * Backward of the FP8 forward (sparton_fwd_fp8): the same argmax-routed
+ * gradients with the e4m3 operands the forward multiplied — H8 [B*S, D] and
+ * E8 [V, D] e4m3 bytes with their per-tensor amax (device f32 scalars; the
+ * dequantised value is q * amax / 448).  dE = sum_b g * Hdq[b, I], dH =
+ * sum_v g * Edq[v] (the straight-through gradient of the FP8 forward), db as
+ * sparton_bwd.  Gathers move half the bytes of the bf16 backward.  Needs
+ * D % 16 == 0 and S <= 832 (the staged dE); workspace as sparton_bwd.
+ * No reference counterpart (PAPER.md:375 lists FP8 as future work).
+ */
+SPARTON_API int sparton_bwd_fp8(const void* H8, const void* E8, const float* amax_h, const float* amax_e,
+                const float* Y, const int32_t* I, const float* dY, void* dH, void* dE, float* db,
+                int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int64_t ldDY,
+                int include_bias_grad, int grad_dtype,
+                void* workspace, size_t workspace_bytes, void* stream, void* dh_ready_event);
+
 #ifdef __cplusplus
 }
 #endif

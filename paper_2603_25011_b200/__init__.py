@@ -11,13 +11,17 @@ Public surface:
   * vocab-sharded multi-GPU head: ``paper_2603_25011_b200.sharded``
 """
 
-from .head import (SpartonHeadFn, bwd_workspace_bytes, quantize_e4m3, sparton_backward, sparton_backward_fp32,
-                   sparton_forward, sparton_forward_fp8, sparton_forward_fp32, sparton_head, split_bf16x3)
+from .head import (SpartonHeadFn, SpartonHeadFp8Fn, bwd_workspace_bytes, quantize_e4m3, sparton_backward,
+                   sparton_backward_fp8, sparton_backward_fp32, sparton_forward, sparton_forward_fp8,
+                   sparton_forward_fp32, sparton_head, sparton_head_fp8, split_bf16x3)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "SpartonHeadFn",
+    "SpartonHeadFp8Fn",
+    "sparton_backward_fp8",
+    "sparton_head_fp8",
     "bwd_workspace_bytes",
     "sparton_backward",
     "sparton_backward_fp32",

@@ -44,6 +44,7 @@ EXPORTED = (
     "sparton_bwd_workspace_bytes",
     "sparton_bwd",
     "sparton_bwd_ex",
+    "sparton_bwd_fp8",
 )
 
 _lock = threading.Lock()
@@ -93,6 +94,8 @@ def load() -> ctypes.CDLL:
                                     c_int, c_int, c_vp, ctypes.c_size_t, c_vp]
         lib.sparton_bwd_ex.restype = c_int
         lib.sparton_bwd_ex.argtypes = lib.sparton_bwd.argtypes + [c_vp]
+        lib.sparton_bwd_fp8.restype = c_int
+        lib.sparton_bwd_fp8.argtypes = [c_vp] * 10 + [c_i64] * 6 + [c_int, c_int, c_vp, ctypes.c_size_t, c_vp, c_vp]
         _lib = lib
         return lib
 

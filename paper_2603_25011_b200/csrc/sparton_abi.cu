@@ -105,6 +105,11 @@ const char* dev_env(const char* name) {
   return getenv(name);
 }
 
+int encode_u8_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long long cols, int box_rows,
+                       int box_cols) {
+  return encode_2d(map, ptr, rows, cols, box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_NONE, true);
+}
+
 int set_error(int code, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
   return code;
@@ -273,10 +278,10 @@ int sparton_bwd(const void* H, const void* E, const float* Y, const int32_t* I, 
                         workspace, workspace_bytes, stream, nullptr);
 }
 
-int sparton_bwd_ex(const void* H, const void* E, const float* Y, const int32_t* I, const float* dY,
-                   void* dH, void* dE, float* db, int64_t B, int64_t S, int64_t D, int64_t V,
-                   int64_t ldY, int64_t ldDY, int include_bias_grad, int grad_dtype, void* workspace,
-                   size_t workspace_bytes, void* stream, void* dh_ready_event) {
+static int bwd_common(const void* H, const void* E, const float* amax_h, const float* amax_e, const float* Y,
+                      const int32_t* I, const float* dY, void* dH, void* dE, float* db, int64_t B, int64_t S,
+                      int64_t D, int64_t V, int64_t ldY, int64_t ldDY, int include_bias_grad, int grad_dtype,
+                      void* workspace, size_t workspace_bytes, void* stream, void* dh_ready_event, bool fp8) {
   int rc = check_dims(B, S, D, V);
   if (rc) return rc;
   if (!H || !E || !Y || !I || !dY || !dH || !dE || !workspace)
@@ -287,6 +292,12 @@ int sparton_bwd_ex(const void* H, const void* E, const float* Y, const int32_t* 
   if (grad_dtype != SPARTON_F32 && grad_dtype != SPARTON_BF16)
     return set_error(SPARTON_EINVAL, "grad_dtype must be SPARTON_F32 or SPARTON_BF16");
   if (S > bwd_max_seq()) return set_error(SPARTON_EINVAL, "S exceeds the backward's routing limit");
+  if (fp8) {
+    if (!amax_h || !amax_e) return set_error(SPARTON_EINVAL, "null amax pointer");
+    if (D % 16 != 0) return set_error(SPARTON_EINVAL, "e4m3 operands need D to be a multiple of 16");
+    if (de_staged_rows((int)S) == 0)
+      return set_error(SPARTON_EINVAL, "the FP8 backward supports S <= 832 (staged dE)");
+  }
   const BwdWorkspace ws = bwd_workspace_layout(B, S, D, V, grad_dtype);
   const size_t need = ws.total;
   if (workspace_bytes < need) {
@@ -324,12 +335,34 @@ int sparton_bwd_ex(const void* H, const void* E, const float* Y, const int32_t* 
   p.gi = ws.de_staged ? reinterpret_cast<int2*>(wsb + ws.gi) : nullptr;
   p.ldGI = ws.ldGI;
   p.dh_ready = static_cast<cudaEvent_t>(dh_ready_event);
+  p.fp8 = fp8 ? 1 : 0;
+  p.amax_h = amax_h;
+  p.amax_e = amax_e;
   CUtensorMap tmH;
   if (ws.de_staged) {
     const int rows = de_staged_rows((int)S);
-    if ((rc = encode_bf16_2d_plain(&tmH, H, B * S, D, rows > 256 ? 256 : rows, 64))) return rc;
+    rc = fp8 ? encode_u8_2d_plain(&tmH, H, B * S, D, rows > 256 ? 256 : rows, 128)
+             : encode_bf16_2d_plain(&tmH, H, B * S, D, rows > 256 ? 256 : rows, 64);
+    if (rc) return rc;
   }
   return launch_bwd(p, ws.de_staged ? &tmH : nullptr, grad_dtype, static_cast<cudaStream_t>(stream));
+}
+
+
+int sparton_bwd_ex(const void* H, const void* E, const float* Y, const int32_t* I, const float* dY,
+                   void* dH, void* dE, float* db, int64_t B, int64_t S, int64_t D, int64_t V,
+                   int64_t ldY, int64_t ldDY, int include_bias_grad, int grad_dtype, void* workspace,
+                   size_t workspace_bytes, void* stream, void* dh_ready_event) {
+  return bwd_common(H, E, nullptr, nullptr, Y, I, dY, dH, dE, db, B, S, D, V, ldY, ldDY, include_bias_grad,
+                    grad_dtype, workspace, workspace_bytes, stream, dh_ready_event, false);
+}
+
+int sparton_bwd_fp8(const void* H8, const void* E8, const float* amax_h, const float* amax_e, const float* Y,
+                    const int32_t* I, const float* dY, void* dH, void* dE, float* db, int64_t B, int64_t S,
+                    int64_t D, int64_t V, int64_t ldY, int64_t ldDY, int include_bias_grad, int grad_dtype,
+                    void* workspace, size_t workspace_bytes, void* stream, void* dh_ready_event) {
+  return bwd_common(H8, E8, amax_h, amax_e, Y, I, dY, dH, dE, db, B, S, D, V, ldY, ldDY, include_bias_grad,
+                    grad_dtype, workspace, workspace_bytes, stream, dh_ready_event, true);
 }
 
 }  // extern "C"

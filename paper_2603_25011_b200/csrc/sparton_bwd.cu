@@ -40,6 +40,7 @@
 #include <cstdlib>
 
 #include <mutex>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -93,6 +94,47 @@ __device__ __forceinline__ void fma8(float* acc, uint64_t gg, const int4& raw) {
         : "r"(w[i]), "l"(gg));
   }
 }
+
+// FP8 operands (sparton_bwd_fp8): acc[0..7] += g * e4m3x8(raw), exact e4m3 ->
+// f16 -> f32 conversions (F2FP.F16.E4M3.UNPACK_B + HADD2.F32), then FFMA2.
+__device__ __forceinline__ void fma4_e4m3(float* acc, uint64_t gg, uint32_t w) {
+  asm("{\n.reg .b16 p0, p1, a0, a1, a2, a3;\n.reg .b32 h0, h1;\n.reg .f32 f0, f1, f2, f3;\n"
+      ".reg .b64 x0, x1, c0, c1;\n"
+      "mov.b32 {p0, p1}, %4;\n"
+      "cvt.rn.f16x2.e4m3x2 h0, p0;\n"
+      "cvt.rn.f16x2.e4m3x2 h1, p1;\n"
+      "mov.b32 {a0, a1}, h0;\n"
+      "mov.b32 {a2, a3}, h1;\n"
+      "cvt.f32.f16 f0, a0;\n"
+      "cvt.f32.f16 f1, a1;\n"
+      "cvt.f32.f16 f2, a2;\n"
+      "cvt.f32.f16 f3, a3;\n"
+      "mov.b64 x0, {f0, f1};\n"
+      "mov.b64 x1, {f2, f3};\n"
+      "mov.b64 c0, {%0, %1};\n"
+      "mov.b64 c1, {%2, %3};\n"
+      "fma.rn.f32x2 c0, x0, %5, c0;\n"
+      "fma.rn.f32x2 c1, x1, %5, c1;\n"
+      "mov.b64 {%0, %1}, c0;\n"
+      "mov.b64 {%2, %3}, c1;\n}\n"
+      : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3])
+      : "r"(w), "l"(gg));
+}
+
+__device__ __forceinline__ void fma8_e4m3(float* acc, uint64_t gg, const uint2& raw) {
+  fma4_e4m3(acc, gg, raw.x);
+  fma4_e4m3(acc + 4, gg, raw.y);
+}
+
+__device__ __forceinline__ void fma16_e4m3(float* acc, uint64_t gg, const int4& raw) {
+  fma4_e4m3(acc, gg, (uint32_t)raw.x);
+  fma4_e4m3(acc + 4, gg, (uint32_t)raw.y);
+  fma4_e4m3(acc + 8, gg, (uint32_t)raw.z);
+  fma4_e4m3(acc + 12, gg, (uint32_t)raw.w);
+}
+
+// Dequantisation scale of an e4m3 operand (amax / 448), or 1 for bf16.
+__device__ __forceinline__ float dq_scale(const float* amax) { return amax ? __ldg(amax) * (1.0f / 448.0f) : 1.0f; }
 
 template <typename OutT>
 __device__ __forceinline__ void store8(OutT* dst, const float* acc);
@@ -359,14 +401,16 @@ int de_cluster(int S) {
   }
   return ((S + 1) / 2 + 7) / 8 * 8 <= 256 ? 2 : 4;
 }
-constexpr int DEST_DD = 64;
-
-template <int NW, int J>
+// A staged row is 128 B: 64 bf16 or (FP8) 128 e4m3 columns of D; each of the
+// 8 lanes of a row group owns 16 B of it (8 or 16 accumulators per row).
+template <int NW, int J, bool FP8 = false>
 struct DeStCfg {
   static constexpr int THREADS = (NW + 1) * 32;
   static constexpr int GROUPS = NW * 4;       // 8-lane groups, one vocab row each per step
   static constexpr int VB = GROUPS * J;       // vocab rows per CTA
   static constexpr int GI_BYTES = VB * 8;
+  static constexpr int DD = FP8 ? 128 : 64;   // D columns per work item
+  static constexpr int AW = FP8 ? 16 : 8;     // accumulators per (lane, vocab row)
 };
 
 __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* m, uint32_t dst, uint32_t bar, int32_t c0,
@@ -378,11 +422,11 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* m, uint32_t ds
       : "memory");
 }
 
-template <int NW, int J, int CL, typename OutT>
-__global__ void __launch_bounds__(DeStCfg<NW, J>::THREADS, 1)
+template <int NW, int J, int CL, typename OutT, bool FP8 = false>
+__global__ void __launch_bounds__(DeStCfg<NW, J, FP8>::THREADS, 1)
 sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdParams p, int R, int nst,
                              int stage_bytes, int nvg, int nitems) {
-  using C = DeStCfg<NW, J>;
+  using C = DeStCfg<NW, J, FP8>;
   extern __shared__ __align__(128) uint8_t ds_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(ds_smem + (size_t)nst * stage_bytes);
   uint64_t* empty = full + nst;
@@ -424,7 +468,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
       uint32_t ph = 0;
       for (int it = cl; it < nitems; it += ncl) {
       const int v0 = ((it % nvg) * CL + (int)crank) * C::VB;
-      const int d0 = (it / nvg) * DEST_DD;
+      const int d0 = (it / nvg) * C::DD;
       const long long vrem = (long long)p.ldGI - v0;          // even
       const uint32_t gi_bytes = (uint32_t)(vrem >= C::VB ? C::GI_BYTES : (vrem > 0 ? vrem * 8 : 0));
       for (int b = 0; b < p.B; ++b) {
@@ -450,12 +494,12 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
     uint32_t ph = 0;
     for (int it = cl; it < nitems; it += ncl) {
     const int v0 = ((it % nvg) * CL + (int)crank) * C::VB;
-    const int d0 = (it / nvg) * DEST_DD;
-    float acc[J][8];
+    const int d0 = (it / nvg) * C::DD;
+    float acc[J][C::AW];
 #pragma unroll
     for (int j = 0; j < J; ++j)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+      for (int i = 0; i < C::AW; ++i) acc[j][i] = 0.f;
     for (int b = 0; b < p.B; ++b) {
       ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
       const uint8_t* tile = ds_smem + (size_t)st * stage_bytes;
@@ -466,7 +510,8 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
       for (int j = 0; j < J; ++j) {
         const int2 e = gi[C::GROUPS * j];
         const int4 x = *reinterpret_cast<const int4*>(rows + e.x * 128);
-        fma8(acc[j], pack_gg(__int_as_float(e.y)), x);
+        if constexpr (FP8) fma16_e4m3(acc[j], pack_gg(__int_as_float(e.y)), x);
+        else fma8(acc[j], pack_gg(__int_as_float(e.y)), x);
       }
       // Every lane's shared loads have been consumed by its FMAs (retired), so a
       // relaxed arrival (no MEMBAR) suffices to release the stage to the
@@ -475,12 +520,22 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
       if (lane < CL) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&empty[st]), (uint32_t)lane));
       if (++st == nst) { st = 0; ph ^= 1; }
     }
-    const int d = d0 + sub * 8;
+    const int d = d0 + sub * C::AW;
     if (d < p.D) {
+      // FP8: dE = (amax_h / 448) * sum_b g * q_h, scaled once per element.
+      const float sc = FP8 ? dq_scale(p.amax_h) : 1.0f;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const int v = v0 + grp + C::GROUPS * j;
-        if (v < p.V) store8<OutT>(reinterpret_cast<OutT*>(p.dE) + (size_t)v * p.D + d, acc[j]);
+        if (v < p.V) {
+          if constexpr (FP8) {
+#pragma unroll
+            for (int i = 0; i < C::AW; ++i) acc[j][i] *= sc;
+          }
+#pragma unroll
+          for (int h = 0; h < C::AW; h += 8)
+            if (d + h < p.D) store8<OutT>(reinterpret_cast<OutT*>(p.dE) + (size_t)v * p.D + d + h, acc[j] + h);
+        }
       }
     }
     }  // items
@@ -699,9 +754,13 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
 // each in ascending v, so the accumulation order is exactly the reference's
 // (v ascending, hidden_row / np.add.at).  Partial sums carry across launches in
 // fp32 (the output itself when it is fp32, else the workspace accumulator).
-template <int CPL, int DH_UNROLL, int MINB, bool FULL, typename OutT, int THREADS = DH_THREADS>
+template <int CPL, int DH_UNROLL, int MINB, bool FULL, typename OutT, int THREADS = DH_THREADS, bool FP8 = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
+  // Lane l owns columns d0 + c*256 + l*8 .. +8 of its row (bf16: one 16-B
+  // load per chunk c; FP8: one 8-B load of e4m3 bytes).
+  using XT = typename std::conditional<FP8, uint2, int4>::type;
+  constexpr int EB = FP8 ? 1 : 2;   // bytes per E element
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long nrows = (long long)p.B * p.S;
@@ -777,37 +836,47 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
     int j = 0;
     for (; j + DH_UNROLL <= m; j += DH_UNROLL) {
       float gq[DH_UNROLL];
-      int4 xq[DH_UNROLL][CPL];
+      XT xq[DH_UNROLL][CPL];
 #pragma unroll
       for (int q = 0; q < DH_UNROLL; ++q) {
         const int vq = __shfl_sync(0xffffffffu, mine.x, j + q);
         gq[q] = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j + q));
-        const __nv_bfloat16* r = p.E + (size_t)vq * p.D + d0 + lane * 8;
+        const uint8_t* r = reinterpret_cast<const uint8_t*>(p.E) + ((size_t)vq * p.D + d0 + lane * 8) * EB;
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
-          xq[q][c] = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
+          xq[q][c] = dvalid[c] ? __ldg(reinterpret_cast<const XT*>(r + c * 256 * EB)) : XT{};
       }
 #pragma unroll
       for (int q = 0; q < DH_UNROLL; ++q) {
         const uint64_t gg = pack_gg(gq[q]);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) fma8(&acc[c * 8], gg, xq[q][c]);
+        for (int c = 0; c < CPL; ++c) {
+          if constexpr (FP8) fma8_e4m3(&acc[c * 8], gg, xq[q][c]);
+          else fma8(&acc[c * 8], gg, xq[q][c]);
+        }
       }
     }
     for (; j < m; ++j) {
       const int va = __shfl_sync(0xffffffffu, mine.x, j);
       const float ga = __int_as_float(__shfl_sync(0xffffffffu, mine.y, j));
-      const __nv_bfloat16* r = p.E + (size_t)va * p.D + d0 + lane * 8;
+      const uint8_t* r = reinterpret_cast<const uint8_t*>(p.E) + ((size_t)va * p.D + d0 + lane * 8) * EB;
       const uint64_t gg = pack_gg(ga);
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        const int4 x = dvalid[c] ? __ldg(reinterpret_cast<const int4*>(r + c * 256)) : make_int4(0, 0, 0, 0);
-        fma8(&acc[c * 8], gg, x);
+        const XT x = dvalid[c] ? __ldg(reinterpret_cast<const XT*>(r + c * 256 * EB)) : XT{};
+        if constexpr (FP8) fma8_e4m3(&acc[c * 8], gg, x);
+        else fma8(&acc[c * 8], gg, x);
       }
     }
   }
 
   if (last) {
+    if constexpr (FP8) {
+      // dH = (amax_e / 448) * sum_v g * q_e, scaled once per element.
+      const float sc = dq_scale(p.amax_e);
+#pragma unroll
+      for (int i = 0; i < CPL * 8; ++i) acc[i] *= sc;
+    }
     OutT* dst = reinterpret_cast<OutT*>(p.dH) + (size_t)rowid * p.D + d0 + lane * 8;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
@@ -928,7 +997,7 @@ int launch_route(const BwdParams& p, cudaStream_t stream) {
   return SPARTON_OK;
 }
 
-template <int CPL, typename OutT>
+template <int CPL, typename OutT, bool FP8 = false>
 int launch_dh(const BwdParams& p, cudaStream_t stream) {
   // Persistent: one 640-thread CTA per SM (20 warps x 4 E rows in flight,
   // 96 registers); warps stride over rows independently, so no warp slot
@@ -944,9 +1013,11 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
   const dim3 grid(sms, dslices);
   for (int c = 0; c < p.nchunks; ++c) {
     if (full)
-      sparton_bwd_dh_kernel<CPL, 4, 1, true, OutT, DH_PERSIST_THREADS><<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
+      sparton_bwd_dh_kernel<CPL, 4, 1, true, OutT, DH_PERSIST_THREADS, FP8>
+          <<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
     else
-      sparton_bwd_dh_kernel<CPL, 4, 1, false, OutT, DH_PERSIST_THREADS><<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
+      sparton_bwd_dh_kernel<CPL, 4, 1, false, OutT, DH_PERSIST_THREADS, FP8>
+          <<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
   }
@@ -955,27 +1026,27 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
 
 constexpr int DEST_SMEM_BUDGET = 227 * 1024;
 
-template <int NW, int J>
+template <int NW, int J, bool FP8 = false>
 int de_stage_bytes_t(int CL, int R) {
-  return (128 + CL * R * 128 + DeStCfg<NW, J>::GI_BYTES + 127) & ~127;
+  return (128 + CL * R * 128 + DeStCfg<NW, J, FP8>::GI_BYTES + 127) & ~127;
 }
 constexpr int DEST_NW = 15, DEST_J = 12;   // 720 vocab rows x 64 columns per CTA (128 regs)
 int de_stage_bytes(int CL, int R) { return de_stage_bytes_t<DEST_NW, DEST_J>(CL, R); }
 
-template <int NW, int J, int CL, typename OutT>
+template <int NW, int J, int CL, typename OutT, bool FP8 = false>
 int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
-  using C = DeStCfg<NW, J>;
+  using C = DeStCfg<NW, J, FP8>;
   const int R = de_staged_rows(p.S);
-  const int stage_bytes = de_stage_bytes_t<NW, J>(CL, R);
+  const int stage_bytes = de_stage_bytes_t<NW, J, FP8>(CL, R);
   int nst = (DEST_SMEM_BUDGET - 128) / stage_bytes;
   if (nst > 4) nst = 4;
   const int smem = nst * stage_bytes + nst * 16;
-  auto kern = sparton_bwd_de_staged_kernel<NW, J, CL, OutT>;
+  auto kern = sparton_bwd_de_staged_kernel<NW, J, CL, OutT, FP8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de_staged)", e);
   const int nvb = (p.V + C::VB - 1) / C::VB;
   const int nvg = (nvb + CL - 1) / CL;
-  const int nitems = nvg * ((p.D + DEST_DD - 1) / DEST_DD);
+  const int nitems = nvg * ((p.D + C::DD - 1) / C::DD);
   int ncl = nitems;
   if (const char* ev = dev_env("SPARTON_DE_CLUSTERS")) {   // persistent grid (SM partition experiments)
     const int n = atoi(ev);
@@ -1004,11 +1075,16 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
 // Register budget split between accumulators (reuse: VB vocab rows per staged
 // H tile) and loads in flight (latency hiding): 15 consumer warps x 12 rows at
 // 128 registers measured 7% faster than 11 x 17 at 168.
-template <typename OutT>
+// FP8: 128 e4m3 columns per staged row and 16 accumulators per (lane, row),
+// so 6 rows per 8-lane group keep the same 96 accumulator registers.
+constexpr int DEST_J_FP8 = 6;
+
+template <typename OutT, bool FP8 = false>
 int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
-  if (de_cluster(p.S) == 1) return launch_de_staged_t<DEST_NW, DEST_J, 1, OutT>(p, tmH, stream);
-  if (de_cluster(p.S) == 2) return launch_de_staged_t<DEST_NW, DEST_J, 2, OutT>(p, tmH, stream);
-  return launch_de_staged_t<DEST_NW, DEST_J, 4, OutT>(p, tmH, stream);
+  constexpr int J = FP8 ? DEST_J_FP8 : DEST_J;
+  if (de_cluster(p.S) == 1) return launch_de_staged_t<DEST_NW, J, 1, OutT, FP8>(p, tmH, stream);
+  if (de_cluster(p.S) == 2) return launch_de_staged_t<DEST_NW, J, 2, OutT, FP8>(p, tmH, stream);
+  return launch_de_staged_t<DEST_NW, J, 4, OutT, FP8>(p, tmH, stream);
 }
 
 template <int CPL, int W, typename OutT>
@@ -1042,6 +1118,16 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
     if ((e = cudaStreamWaitEvent(stream, ss.join, 0)) != cudaSuccess) return set_cuda_error("join side stream", e);
     return SPARTON_OK;
   };
+  if (p.fp8) {
+    // FP8 operands (staged dE only; the ABI checks S): route, then dE || dH.
+    if (p.gi == nullptr) return set_error(SPARTON_EINVAL, "the FP8 backward needs the staged dE (S <= 832)");
+    if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
+    if ((rc = fork()) != SPARTON_OK) return rc;
+    if ((rc = launch_de_staged<OutT, true>(p, tmH, ss.s)) != SPARTON_OK) return rc;
+    if ((rc = launch_dh<CPL, OutT, true>(p, stream)) != SPARTON_OK) return rc;
+    if ((rc = dh_done()) != SPARTON_OK) return rc;
+    return join();
+  }
   if (p.gi != nullptr) {
     // Staged dE needs the route's (s, g) records: route, then dE || dH.
     if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;

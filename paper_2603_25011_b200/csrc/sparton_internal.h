@@ -65,6 +65,11 @@ struct BwdParams {
   int2* gi;            // workspace: per-(b, v) (s, g) records, row stride ldGI (staged dE), or nullptr
   long long ldGI;      // even row stride of gi (16-B aligned rows)
   cudaEvent_t dh_ready; // optional: recorded on the caller's stream once dH is final (before dE joins)
+  // FP8 backward (sparton_bwd_fp8): H and E are e4m3 bytes (H, E point at
+  // them), dequantised by amax/448 (device scalars) once per output element.
+  int fp8;
+  const float* amax_h;
+  const float* amax_e;
 };
 
 // Workspace layout for sparton_bwd (byte offsets, 256-B aligned).
@@ -95,6 +100,9 @@ int fwd_h_box_rows(int cluster_ctas);
 int encode_bf16_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long long cols, int box_rows,
                          int box_cols);
 int launch_bwd(const BwdParams& prm, const CUtensorMap* tmH, int grad_dtype, cudaStream_t stream);
+// H viewed as (B*S) x D bytes with a (128 x rows) box, no swizzle (FP8 staged dE tiles).
+int encode_u8_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long long cols, int box_rows,
+                       int box_cols);
 // Rows of H each CTA of a staged-dE cluster loads per batch row (0: staged dE unsupported for S).
 int de_staged_rows(int S);
 int bwd_max_seq();

@@ -25,6 +25,9 @@ __all__ = [
     "sparton_backward",
     "sparton_forward_fp32",
     "sparton_backward_fp32",
+    "sparton_backward_fp8",
+    "SpartonHeadFp8Fn",
+    "sparton_head_fp8",
     "split_bf16x3",
     "SpartonHeadFn",
     "sparton_head",
@@ -143,15 +146,16 @@ def quantize_e4m3(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
 
 @torch.no_grad()
 def sparton_forward_fp8(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor, *,
-                        E_q: tuple[torch.Tensor, torch.Tensor] | None = None, cta_group: int = 0
-                        ) -> tuple[torch.Tensor, torch.Tensor]:
+                        E_q: tuple[torch.Tensor, torch.Tensor] | None = None, cta_group: int = 0,
+                        return_quantized: bool = False):
     """FP8 (e4m3) variant of the fused forward — tcgen05 kind::f8f6f4 at twice
     the bf16 tensor rate; the paper's future-work item.
 
     H and E (bf16) are quantised per tensor on the GPU (``E_q`` may pass a
     cached ``quantize_e4m3(E)``).  Y/I follow the same definition as
     ``sparton_forward`` on the dequantised operands; they are approximate
-    relative to bf16 (e4m3 keeps 3 mantissa bits)."""
+    relative to bf16 (e4m3 keeps 3 mantissa bits).  ``return_quantized``
+    also returns (qH, amax_h, qE, amax_e) for ``sparton_backward_fp8``."""
     B, S, D, V = _check_inputs(H, E, bias, mask)
     if D % 16:
         raise ValueError("the e4m3 forward needs D to be a multiple of 16")
@@ -163,13 +167,69 @@ def sparton_forward_fp8(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, ma
     bias = bias.contiguous()
     Y = torch.empty((B, V), dtype=torch.float32, device=H.device)
     I = torch.empty((B, V), dtype=torch.int32, device=H.device)
+    out = _fwd_fp8_launch(qH, aH, qE, aE, bias, m, Y, I, cta_group)
+    return (out, (qH, aH, qE, aE)) if return_quantized else out
+
+
+def _fwd_fp8_launch(qH, aH, qE, aE, bias, m, Y, I, cta_group=0):
+    B, V = Y.shape
+    S, D = qH.shape[1], qH.shape[2]
     lib = _lib.load()
-    with torch.cuda.device(H.device):
+    with torch.cuda.device(qH.device):
         rc = lib.sparton_fwd_fp8(qH.data_ptr(), qE.data_ptr(), aH.data_ptr(), aE.data_ptr(), bias.data_ptr(),
                                  m.data_ptr(), Y.data_ptr(), I.data_ptr(), B, S, D, V, V, int(cta_group),
                                  _stream_ptr())
     _lib.check(rc)
     return Y, I
+
+
+@torch.no_grad()
+def sparton_backward_fp8(qH: torch.Tensor, amax_h: torch.Tensor, qE: torch.Tensor, amax_e: torch.Tensor,
+                         Y: torch.Tensor, I: torch.Tensor, dY: torch.Tensor, *, include_bias_grad: bool = True,
+                         grad_dtype: torch.dtype = torch.bfloat16
+                         ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Backward of the FP8 forward: the argmax-routed gradients with the e4m3
+    operands the forward multiplied (``quantize_e4m3`` outputs: qH [B,S,D]
+    and qE [V,D] bytes, amax scalars; value = q * amax / 448).  dE gathers
+    staged e4m3 H rows and dH gathers e4m3 E rows — half the bytes of the
+    bf16 backward — with fp32 accumulation in the reference's order, and the
+    dequantisation scale applied once per output element.  This is the
+    straight-through gradient of ``sparton_forward_fp8``; S <= 832."""
+    for name, t in (("qH", qH), ("qE", qE), ("amax_h", amax_h), ("amax_e", amax_e), ("Y", Y), ("I", I),
+                    ("dY", dY)):
+        _require_cuda(name, t)
+    if qH.dim() != 3 or qE.dim() != 2 or qE.shape[1] != qH.shape[2]:
+        raise ValueError("qH must be (B, S, D) and qE (V, D)")
+    if qH.dtype != torch.uint8 or qE.dtype != torch.uint8:
+        raise ValueError("qH and qE must hold e4m3 bytes (uint8, from quantize_e4m3)")
+    B, S, D = qH.shape
+    V = qE.shape[0]
+    if Y.shape != (B, V) or I.shape != (B, V) or dY.shape != (B, V):
+        raise ValueError(f"saved state and dY must have shape {(B, V)}")
+    if Y.dtype != torch.float32 or I.dtype != torch.int32 or dY.dtype != torch.float32:
+        raise ValueError("Y/dY must be float32 and I int32")
+    if grad_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("grad_dtype must be torch.float32 or torch.bfloat16")
+    qH, qE = qH.contiguous(), qE.contiguous()
+    if Y.stride(1) != 1 or I.stride(1) != 1 or I.stride(0) != Y.stride(0) or Y.stride(0) < V:
+        Y, I = Y.contiguous(), I.contiguous()
+    if dY.stride(1) != 1 or dY.stride(0) < V:
+        dY = dY.contiguous()
+    dev = qH.device
+    dH = torch.empty((B, S, D), dtype=grad_dtype, device=dev)
+    dE = torch.empty((V, D), dtype=grad_dtype, device=dev)
+    db = torch.empty((V,), dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    gd = _lib.SPARTON_BF16 if grad_dtype == torch.bfloat16 else _lib.SPARTON_F32
+    ws_bytes = int(lib.sparton_bwd_workspace_bytes(B, S, D, V, gd))
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        rc = lib.sparton_bwd_fp8(qH.data_ptr(), qE.data_ptr(), amax_h.data_ptr(), amax_e.data_ptr(), Y.data_ptr(),
+                                 I.data_ptr(), dY.data_ptr(), dH.data_ptr(), dE.data_ptr(), db.data_ptr(), B, S, D,
+                                 V, Y.stride(0), dY.stride(0), int(bool(include_bias_grad)), gd, ws.data_ptr(),
+                                 ws_bytes, _stream_ptr(), None)
+    _lib.check(rc)
+    return dH, dE, db
 
 
 def bwd_workspace_bytes(B: int, S: int, D: int, V: int, grad_dtype: torch.dtype = torch.float32) -> int:
@@ -333,6 +393,38 @@ class SpartonHeadFn(torch.autograd.Function):
         if dE.dtype != E.dtype:
             dE = dE.to(E.dtype)
         return dH, dE, db, None, None
+
+
+class SpartonHeadFp8Fn(torch.autograd.Function):
+    """FP8 autograd op: the e4m3 forward (``sparton_forward_fp8``) saves the
+    quantised operands with (Y, I); backward is ``sparton_backward_fp8``
+    (straight-through w.r.t. the quantisation).  Gradients in the inputs'
+    dtypes (bf16 for H/E, f32 for bias)."""
+
+    @staticmethod
+    def forward(ctx, H, E, bias, mask, include_bias_grad=True):
+        (Y, I), (qH, aH, qE, aE) = sparton_forward_fp8(H, E, bias, mask, return_quantized=True)
+        ctx.save_for_backward(qH, aH, qE, aE, Y, I)
+        ctx.include_bias_grad = bool(include_bias_grad)
+        ctx.dtypes = (H.dtype, E.dtype)
+        ctx.mark_non_differentiable(I)
+        return Y, I
+
+    @staticmethod
+    def backward(ctx, dY, dI_unused):
+        qH, aH, qE, aE, Y, I = ctx.saved_tensors
+        if dY is None:
+            return None, None, None, None, None
+        dH, dE, db = sparton_backward_fp8(qH, aH, qE, aE, Y, I, dY.float(),
+                                          include_bias_grad=ctx.include_bias_grad, grad_dtype=ctx.dtypes[0])
+        return dH, dE.to(ctx.dtypes[1]), db, None, None
+
+
+def sparton_head_fp8(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,
+                     *, return_indices: bool = False, include_bias_grad: bool = True):
+    """FP8 (e4m3, per-tensor scales) forward + backward of the head."""
+    Y, I = SpartonHeadFp8Fn.apply(H, E, bias, mask, include_bias_grad)
+    return (Y, I) if return_indices else Y
 
 
 def sparton_head(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,

@@ -23,7 +23,8 @@ def test_header_declares_entry_points():
     names = _declared()
     assert names == sorted(["sparton_abi_version", "sparton_last_error", "sparton_device_sm_count",
                             "sparton_fwd", "sparton_fwd_fp8", "sparton_fwd_multi", "sparton_quantize_e4m3",
-                            "sparton_bwd_workspace_bytes", "sparton_bwd", "sparton_bwd_ex"])
+                            "sparton_bwd_workspace_bytes", "sparton_bwd", "sparton_bwd_ex",
+                            "sparton_bwd_fp8"])
 
 
 def test_library_exports_every_declared_symbol():

@@ -64,3 +64,70 @@ def test_fp8_vs_bf16_gap_is_small(cuda_device):
     agree = float((I8 == I16).float().mean())
     print(f"fp8 vs bf16: median rel |dY| {rel:.3e}, argmax agreement {agree:.3f}")
     assert rel < 0.05 and agree > 0.5
+
+
+def _dequant(q, amax):
+    return (q.view(torch.float8_e4m3fn).float() * (float(amax) / 448.0)).cpu().numpy()
+
+
+@pytest.mark.parametrize("dims", [(2, 40, 64, 300), (3, 256, 128, 1000), (4, 512, 768, 3001), (3, 300, 96, 500),
+                                  (2, 832, 64, 700), (5, 17, 1024, 9000)])
+@pytest.mark.parametrize("grad_dtype", [torch.float32, torch.bfloat16])
+def test_fp8_backward_vs_oracle_on_dequantised_operands(cuda_device, dims, grad_dtype):
+    """sparton_backward_fp8 gathers e4m3 rows (staged H tiles for dE, E rows
+    for dH) and scales once per output: it equals the reference backward run
+    on the dequantised operands (the straight-through gradient of the FP8
+    forward) within rtol 1e-2 / atol 1e-3."""
+    from paper_2603_25011_b200 import sparton_backward_fp8, sparton_forward_fp8
+    B, S, D, V = dims
+    H, E, b, m = orc.seeded_inputs(B, S, D, V, 50 + S, mask_keep=0.85)
+    dY = orc.seeded_uniform((B, V), 51)
+    Ht = torch.from_numpy(H).cuda().to(torch.bfloat16)
+    Et = torch.from_numpy(E).cuda().to(torch.bfloat16)
+    (Y, I), (qH, aH, qE, aE) = sparton_forward_fp8(Ht, Et, torch.from_numpy(b).cuda(), torch.from_numpy(m).cuda(),
+                                                   return_quantized=True)
+    dH, dE, db = sparton_backward_fp8(qH, aH, qE, aE, Y, I, torch.from_numpy(dY).cuda(), grad_dtype=grad_dtype)
+    Hd, Ed = _dequant(qH, aH), _dequant(qE, aE)
+    dH_r, dE_r, db_r = orc.backward(Hd, Ed, b, Y.cpu().numpy(), I.cpu().numpy(), dY)
+    for got, want in ((dH, dH_r), (dE, dE_r), (db, db_r)):
+        g = got.float().cpu().numpy()
+        assert np.all(np.abs(g - want) <= 1e-3 + 1e-2 * np.abs(want)), np.max(np.abs(g - want))
+
+
+def test_fp8_backward_guards(cuda_device):
+    from paper_2603_25011_b200 import quantize_e4m3, sparton_backward_fp8
+    qH, aH = quantize_e4m3(torch.ones((2, 900, 64), dtype=torch.bfloat16, device="cuda"))
+    qE, aE = quantize_e4m3(torch.ones((10, 64), dtype=torch.bfloat16, device="cuda"))
+    Y = torch.ones((2, 10), device="cuda")
+    I = torch.zeros((2, 10), dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError, match="832"):
+        sparton_backward_fp8(qH, aH, qE, aE, Y, I, Y)            # S = 900 > 832
+    with pytest.raises(ValueError):
+        sparton_backward_fp8(qH.float(), aH, qE, aE, Y, I, Y)    # not e4m3 bytes
+
+
+def test_fp8_autograd_head_fullsize_rows(cuda_device):
+    """sparton_head_fp8 at cfg3: the bench's FP8 fwd+bwd path, sampled rows
+    and columns vs the oracle on the dequantised operands."""
+    from paper_2603_25011_b200 import quantize_e4m3, sparton_head_fp8
+    g = torch.Generator(device="cuda").manual_seed(7)
+    B, S, D, V = 512, 512, 768, 250002
+    H = torch.randn((B, S, D), generator=g, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    E = (torch.randn((V, D), generator=g, device="cuda") * 0.02).to(torch.bfloat16).requires_grad_(True)
+    b = torch.zeros(V, device="cuda", requires_grad=True)
+    m = torch.ones((B, S), dtype=torch.uint8, device="cuda")
+    dY = torch.randn((B, V), generator=g, device="cuda")
+    Y, I = sparton_head_fp8(H, E, b, m, return_indices=True)
+    Y.backward(dY)
+    torch.cuda.synchronize()
+    qH, aH = quantize_e4m3(H.detach())
+    qE, aE = quantize_e4m3(E.detach())
+    Hd, Ed = _dequant(qH, aH), _dequant(qE, aE)
+    Yn, In, dYn = Y.detach().cpu().numpy(), I.cpu().numpy(), dY.cpu().numpy()
+    rows = [1, 400]
+    dH_r = orc.backward_rows(Hd, Ed, Yn, In, dYn, rows)
+    assert np.all(np.abs(H.grad[rows].float().cpu().numpy() - dH_r) <= 1e-3 + 1e-2 * np.abs(dH_r))
+    cols = np.random.default_rng(1).choice(V, 256, replace=False)
+    dE_r, db_r = orc.backward_cols(Hd, Yn, In, dYn, cols)
+    assert np.all(np.abs(E.grad[cols].float().cpu().numpy() - dE_r) <= 1e-3 + 1e-2 * np.abs(dE_r))
+    assert np.all(np.abs(b.grad[cols].cpu().numpy() - db_r) <= 1e-3 + 1e-2 * np.abs(db_r))
