@@ -159,7 +159,8 @@ SPARTON_API int sparton_bwd_ex(const void* H, const void* E, const float* Y, con
  * E8 [V, D] e4m3 bytes with their per-tensor amax (device f32 scalars; the
  * dequantised value is q * amax / 448).  dE = sum_b g * Hdq[b, I], dH =
  * sum_v g * Edq[v] (the straight-through gradient of the FP8 forward), db as
- * sparton_bwd.  Gathers move half the bytes of the bf16 backward.  Needs
+ * sparton_bwd.  Staged tiles and gathers move half the bytes of the bf16
+ * backward.  Needs
  * D % 16 == 0 and S <= 832 (the staged dE); workspace as sparton_bwd.
  * No reference counterpart (PAPER.md:375 lists FP8 as future work).
  */

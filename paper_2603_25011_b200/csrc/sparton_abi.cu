@@ -341,7 +341,7 @@ static int bwd_common(const void* H, const void* E, const float* amax_h, const f
   CUtensorMap tmH;
   if (ws.de_staged) {
     const int rows = de_staged_rows((int)S);
-    rc = fp8 ? encode_u8_2d_plain(&tmH, H, B * S, D, rows > 256 ? 256 : rows, 128)
+    rc = fp8 ? encode_u8_2d_plain(&tmH, H, B * S, D, rows > 256 ? 256 : rows, 64)
              : encode_bf16_2d_plain(&tmH, H, B * S, D, rows > 256 ? 256 : rows, 64);
     if (rc) return rc;
   }

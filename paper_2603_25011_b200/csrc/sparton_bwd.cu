@@ -54,6 +54,8 @@ namespace {
 constexpr int DE_RPW = 2;       // vocab rows per warp (a CTA of W warps owns 2*W vocab rows)
 constexpr int DH_THREADS = 256;
 constexpr int DH_PERSIST_THREADS = 640;
+constexpr int DH_FP8_THREADS = 512;
+constexpr int DH_FP8_UNROLL = 8;
 
 // A (b, v) pair contributes iff Y > 0 (fused.py:247-249).  An argmax index
 // outside [0, S) (saved state from another forward) is treated as inactive
@@ -401,16 +403,19 @@ int de_cluster(int S) {
   }
   return ((S + 1) / 2 + 7) / 8 * 8 <= 256 ? 2 : 4;
 }
-// A staged row is 128 B: 64 bf16 or (FP8) 128 e4m3 columns of D; each of the
-// 8 lanes of a row group owns 16 B of it (8 or 16 accumulators per row).
+// A staged row holds the item's 64 columns of D: 128 B of bf16, or (FP8)
+// 64 B of e4m3 — half the tile-write and row-read bytes of shared memory for
+// the same 720 vocab rows of fp32 accumulators.  Each of the 8 lanes of a row
+// group owns 8 columns (16 B bf16 / 8 B e4m3) of every row it reads.
 template <int NW, int J, bool FP8 = false>
 struct DeStCfg {
   static constexpr int THREADS = (NW + 1) * 32;
   static constexpr int GROUPS = NW * 4;       // 8-lane groups, one vocab row each per step
   static constexpr int VB = GROUPS * J;       // vocab rows per CTA
   static constexpr int GI_BYTES = VB * 8;
-  static constexpr int DD = FP8 ? 128 : 64;   // D columns per work item
-  static constexpr int AW = FP8 ? 16 : 8;     // accumulators per (lane, vocab row)
+  static constexpr int DD = 64;               // D columns per work item
+  static constexpr int AW = 8;                // accumulators per (lane, vocab row)
+  static constexpr int RB = FP8 ? 64 : 128;   // bytes per staged row
 };
 
 __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* m, uint32_t dst, uint32_t bar, int32_t c0,
@@ -439,7 +444,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
   const int cl = (int)(blockIdx.x / CL), ncl = (int)(gridDim.x / CL);
   // Stage layout: [zero row][S-row tile][GI records].  s = -1 (inactive pair)
   // addresses the zero row, so inactive pairs never touch H.
-  const uint32_t tile_bytes = (uint32_t)(CL * R * 128);
+  const uint32_t tile_bytes = (uint32_t)(CL * R * C::RB);
   const uint32_t gi_off = 128 + tile_bytes;
 
   // Zero rows and GI regions start zeroed / (-1, 0): entries past the
@@ -478,7 +483,7 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
         ptx::mbar_arrive_expect_tx(fb, tile_bytes + gi_bytes);
         // R rows per CTA in boxes of at most 256 rows (the TMA box limit).
         for (int r0 = 0; r0 < R; r0 += 256)
-          tma_load_2d_mc(&tmH, sbase + 128 + (crank * (uint32_t)R + (uint32_t)r0) * 128u, fb, d0,
+          tma_load_2d_mc(&tmH, sbase + 128 + (crank * (uint32_t)R + (uint32_t)r0) * (uint32_t)C::RB, fb, d0,
                          b * p.S + (int)crank * R + r0, (uint16_t)((1u << CL) - 1u), pol);
         if (gi_bytes) bulk_g2s(sbase + gi_off, p.gi + (size_t)b * p.ldGI + v0, gi_bytes, fb);
         if (++st == nst) { st = 0; ph ^= 1; }
@@ -503,15 +508,19 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
     for (int b = 0; b < p.B; ++b) {
       ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
       const uint8_t* tile = ds_smem + (size_t)st * stage_bytes;
-      const uint8_t* rows = tile + 128 + sub * 16;
+      const uint8_t* rows = tile + 128 + sub * (C::RB / 8);
       // Group grp owns vocab rows grp + GROUPS*j: one broadcast record load each.
       const int2* gi = reinterpret_cast<const int2*>(tile + gi_off) + grp;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const int2 e = gi[C::GROUPS * j];
-        const int4 x = *reinterpret_cast<const int4*>(rows + e.x * 128);
-        if constexpr (FP8) fma16_e4m3(acc[j], pack_gg(__int_as_float(e.y)), x);
-        else fma8(acc[j], pack_gg(__int_as_float(e.y)), x);
+        if constexpr (FP8) {
+          const uint2 x = *reinterpret_cast<const uint2*>(rows + e.x * C::RB);
+          fma8_e4m3(acc[j], pack_gg(__int_as_float(e.y)), x);
+        } else {
+          const int4 x = *reinterpret_cast<const int4*>(rows + e.x * C::RB);
+          fma8(acc[j], pack_gg(__int_as_float(e.y)), x);
+        }
       }
       // Every lane's shared loads have been consumed by its FMAs (retired), so a
       // relaxed arrival (no MEMBAR) suffices to release the stage to the
@@ -1012,12 +1021,13 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
   if (e != cudaSuccess) return set_cuda_error("cudaDeviceGetAttribute(dh)", e);
   const dim3 grid(sms, dslices);
   for (int c = 0; c < p.nchunks; ++c) {
+    // FP8 rows are half as wide (8-B loads): 16 warps x 8 rows in flight.
+    constexpr int T = FP8 ? DH_FP8_THREADS : DH_PERSIST_THREADS;
+    constexpr int U = FP8 ? DH_FP8_UNROLL : 4;
     if (full)
-      sparton_bwd_dh_kernel<CPL, 4, 1, true, OutT, DH_PERSIST_THREADS, FP8>
-          <<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
+      sparton_bwd_dh_kernel<CPL, U, 1, true, OutT, T, FP8><<<grid, T, 0, stream>>>(p, c);
     else
-      sparton_bwd_dh_kernel<CPL, 4, 1, false, OutT, DH_PERSIST_THREADS, FP8>
-          <<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, c);
+      sparton_bwd_dh_kernel<CPL, U, 1, false, OutT, T, FP8><<<grid, T, 0, stream>>>(p, c);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
   }
@@ -1028,7 +1038,8 @@ constexpr int DEST_SMEM_BUDGET = 227 * 1024;
 
 template <int NW, int J, bool FP8 = false>
 int de_stage_bytes_t(int CL, int R) {
-  return (128 + CL * R * 128 + DeStCfg<NW, J, FP8>::GI_BYTES + 127) & ~127;
+  using C = DeStCfg<NW, J, FP8>;
+  return (128 + CL * R * C::RB + C::GI_BYTES + 127) & ~127;
 }
 constexpr int DEST_NW = 15, DEST_J = 12;   // 720 vocab rows x 64 columns per CTA (128 regs)
 int de_stage_bytes(int CL, int R) { return de_stage_bytes_t<DEST_NW, DEST_J>(CL, R); }
@@ -1075,13 +1086,9 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
 // Register budget split between accumulators (reuse: VB vocab rows per staged
 // H tile) and loads in flight (latency hiding): 15 consumer warps x 12 rows at
 // 128 registers measured 7% faster than 11 x 17 at 168.
-// FP8: 128 e4m3 columns per staged row and 16 accumulators per (lane, row),
-// so 6 rows per 8-lane group keep the same 96 accumulator registers.
-constexpr int DEST_J_FP8 = 6;
-
 template <typename OutT, bool FP8 = false>
 int launch_de_staged(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream) {
-  constexpr int J = FP8 ? DEST_J_FP8 : DEST_J;
+  constexpr int J = DEST_J;
   if (de_cluster(p.S) == 1) return launch_de_staged_t<DEST_NW, J, 1, OutT, FP8>(p, tmH, stream);
   if (de_cluster(p.S) == 2) return launch_de_staged_t<DEST_NW, J, 2, OutT, FP8>(p, tmH, stream);
   return launch_de_staged_t<DEST_NW, J, 4, OutT, FP8>(p, tmH, stream);

@@ -1,0 +1,74 @@
+"""A/B two builds of libsparton_b200.so on the cfg3 fwd+bwd step, in ONE
+process on one box (alternating A B A B ... to cancel clock drift).  Uses only
+the entry points every build exports (sparton_fwd, sparton_bwd, workspace
+query) through ctypes, so builds from earlier rounds can be compared.
+
+    python tools/ab_step.py build/ab/r01.so build/ab/cur.so [rounds] [steps]
+"""
+import ctypes
+import statistics
+import sys
+
+import torch
+
+libs = [ctypes.CDLL(p) for p in sys.argv[1:3]]
+rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 10
+vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+for lib in libs:
+    lib.sparton_fwd.argtypes = [vp] * 6 + [i64] * 5 + [ci, vp]
+    lib.sparton_bwd_workspace_bytes.argtypes = [i64] * 4 + [ci]
+    lib.sparton_bwd_workspace_bytes.restype = ctypes.c_size_t
+    lib.sparton_bwd.argtypes = [vp] * 8 + [i64] * 6 + [ci, ci, vp, ctypes.c_size_t, vp]
+
+B, S, D, V = 512, 512, 768, 250002
+dev = torch.device("cuda", 0)
+g = torch.Generator(device=dev).manual_seed(0)
+H = torch.randn((B, S, D), generator=g, device=dev).to(torch.bfloat16)
+E = (torch.randn((V, D), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+b = torch.zeros(V, device=dev)
+m = torch.ones((B, S), dtype=torch.uint8, device=dev)
+dY = torch.randn((B, V), generator=g, device=dev)
+Y = torch.empty((B, V), device=dev)
+I = torch.empty((B, V), dtype=torch.int32, device=dev)
+dH = torch.empty((B, S, D), dtype=torch.bfloat16, device=dev)
+dE = torch.empty((V, D), dtype=torch.bfloat16, device=dev)
+db = torch.empty(V, device=dev)
+ws_n = max(int(lib.sparton_bwd_workspace_bytes(B, S, D, V, 1)) for lib in libs)
+ws = torch.empty(ws_n, dtype=torch.uint8, device=dev)
+st = torch.cuda.current_stream().cuda_stream
+
+
+def step(lib, fwd_ev):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    assert lib.sparton_fwd(H.data_ptr(), E.data_ptr(), b.data_ptr(), m.data_ptr(), Y.data_ptr(), I.data_ptr(),
+                           B, S, D, V, V, 0, st) == 0
+    e1.record()
+    fwd_ev.append((e0, e1))
+    assert lib.sparton_bwd(H.data_ptr(), E.data_ptr(), Y.data_ptr(), I.data_ptr(), dY.data_ptr(), dH.data_ptr(),
+                           dE.data_ptr(), db.data_ptr(), B, S, D, V, V, V, 1, 1, ws.data_ptr(), ws_n, st) == 0
+
+
+res = {0: [], 1: []}
+for r in range(rounds):
+    for k, lib in enumerate(libs):
+        fe = []
+        for _ in range(3):
+            step(lib, fe)
+        torch.cuda.synchronize()
+        fe.clear()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            step(lib, fe)
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / steps
+        fwd = statistics.mean(a.elapsed_time(c) for a, c in fe)
+        res[k].append((ms, fwd))
+        print(f"round {r} {sys.argv[1 + k]}: step {ms:.2f} ms  fwd {fwd:.2f}  bwd {ms - fwd:.2f}", flush=True)
+for k in (0, 1):
+    ms = statistics.median(x[0] for x in res[k])
+    fwd = statistics.median(x[1] for x in res[k])
+    print(f"MEDIAN {sys.argv[1 + k]}: step {ms:.2f} fwd {fwd:.2f} bwd {ms - fwd:.2f}")
