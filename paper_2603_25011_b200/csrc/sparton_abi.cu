@@ -338,6 +338,19 @@ static int bwd_common(const void* H, const void* E, const float* amax_h, const f
   p.fp8 = fp8 ? 1 : 0;
   p.amax_h = amax_h;
   p.amax_e = amax_e;
+  // Sparse regime (staged-dE shapes, bf16 operands): thresholds in active
+  // pairs, as a percentage of B*V (tools/sparse_probe.py measured the
+  // crossovers; SPARTON_DE_SPARSE_PCT / SPARTON_DH_SPARSE_PCT override them
+  // under the dev gate, a negative value disables the sparse kernel).
+  if (ws.de_staged && !fp8) {
+    p.stats = reinterpret_cast<unsigned long long*>(wsb + ws.stats);
+    double de_pct = kDeSparsePct, dh_pct = kDhSparsePct;
+    if (const char* ev = dev_env("SPARTON_DE_SPARSE_PCT")) de_pct = atof(ev);
+    if (const char* ev = dev_env("SPARTON_DH_SPARSE_PCT")) dh_pct = atof(ev);
+    const double pairs = (double)B * (double)V;
+    p.de_sparse_max = de_pct < 0 ? -1 : (long long)(pairs * de_pct / 100.0);
+    p.dh_sparse_max = dh_pct < 0 ? -1 : (long long)(pairs * dh_pct / 100.0);
+  }
   CUtensorMap tmH;
   if (ws.de_staged) {
     const int rows = de_staged_rows((int)S);

@@ -70,6 +70,15 @@ __device__ __forceinline__ float pair_grad(float y, float dy) {
   return dy * expf(-y);
 }
 
+// Sparse-regime decisions (BwdParams::stats): every thread of a launch reads
+// the same count, written by the route earlier in stream order.
+__device__ __forceinline__ bool de_sparse(const BwdParams& p) {
+  return p.stats != nullptr && (long long)__ldg(p.stats) <= p.de_sparse_max;
+}
+__device__ __forceinline__ bool dh_sparse(const BwdParams& p) {
+  return p.stats != nullptr && (long long)__ldg(p.stats) <= p.dh_sparse_max;
+}
+
 // acc[0..7] += g * bf16x8(raw), as four packed fp32x2 FMAs (FFMA2: two
 // independent round-to-nearest fp32 FMAs, bit-identical to scalar fmaf).
 // bf16 -> fp32 is exact: the low half of each 32-bit word moves to the top
@@ -432,6 +441,7 @@ __global__ void __launch_bounds__(DeStCfg<NW, J, FP8>::THREADS, 1)
 sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdParams p, int R, int nst,
                              int stage_bytes, int nvg, int nitems) {
   using C = DeStCfg<NW, J, FP8>;
+  if (de_sparse(p)) return;   // uniform over the grid: before any cluster barrier
   extern __shared__ __align__(128) uint8_t ds_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(ds_smem + (size_t)nst * stage_bytes);
   uint64_t* empty = full + nst;
@@ -557,13 +567,88 @@ sparton_bwd_de_staged_kernel(const __grid_constant__ CUtensorMap tmH, const BwdP
 __global__ void __launch_bounds__(256)
 sparton_bwd_db_kernel(const BwdParams p) {
   const int v = blockIdx.x * 256 + threadIdx.x;
-  if (v >= p.V || p.db == nullptr) return;
+  if (v >= p.V || p.db == nullptr || de_sparse(p)) return;
   float s = 0.f;
   if (p.include_bias_grad) {
     const int2* col = p.gi + v;
     for (int b = 0; b < p.B; ++b) s += __int_as_float(__ldg(&col[(size_t)b * p.ldGI].y));
   }
   p.db[v] = s;
+}
+
+// ------------------------------------------------------------------ K2x: sparse dE
+// The sparse regime (at most de_sparse_max active pairs; SPLADE
+// representations are mostly zeros): staging whole H tiles per batch row
+// would pay the dense price for a few pairs.  Warp owns one vocab row v and
+// a slice of 256*CPL columns of D (grid.y; lane l: columns d0 + c*256 + l*8
+// .. +8).  It scans the route's (s, g)
+// records of column v, 32 batch rows per load (lane = b), and gathers
+// H[b, s, :] for the active pairs only, in ascending b (the reference's
+// order, fused.py:255-265), DES_U rows in flight; db[v] is the ascending sum
+// of the same g.  Same fp32 FMA chain per output element as the staged dE
+// (which adds g = 0 times a zero row for inactive pairs).
+constexpr int DES_THREADS = 512;
+constexpr int DES_U = 4;
+
+template <int CPL, bool FULL, typename OutT>
+__global__ void __launch_bounds__(DES_THREADS, 1)
+sparton_bwd_de_sparse_kernel(const BwdParams p) {
+  if (!de_sparse(p)) return;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int d0 = blockIdx.y * (256 * CPL);
+  bool dvalid[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) dvalid[c] = FULL || (d0 + c * 256 + lane * 8) < p.D;
+  const long long nwarps = (long long)gridDim.x * (DES_THREADS / 32);
+  for (long long v = (long long)blockIdx.x * (DES_THREADS / 32) + warp; v < p.V; v += nwarps) {
+    float acc[CPL * 8];
+#pragma unroll
+    for (int i = 0; i < CPL * 8; ++i) acc[i] = 0.f;
+    float gsum = 0.f;
+    const int2* col = p.gi + v;
+    // Records of batch rows b0 + lane and b0 + 32 + lane in flight.
+    int2 r0 = lane < p.B ? __ldg(&col[(size_t)lane * p.ldGI]) : make_int2(-1, 0);
+    int2 r1 = 32 + lane < p.B ? __ldg(&col[(size_t)(32 + lane) * p.ldGI]) : make_int2(-1, 0);
+    for (int b0 = 0; b0 < p.B; b0 += 32) {
+      const int2 rec = r0;
+      r0 = r1;
+      r1 = b0 + 64 + lane < p.B ? __ldg(&col[(size_t)(b0 + 64 + lane) * p.ldGI]) : make_int2(-1, 0);
+      unsigned act = __ballot_sync(0xffffffffu, rec.x >= 0);
+      while (act) {
+        int ln[DES_U];
+        float gq[DES_U];
+        int4 xq[DES_U][CPL];
+#pragma unroll
+        for (int q = 0; q < DES_U; ++q) {
+          ln[q] = act ? __ffs(act) - 1 : -1;
+          act &= act - 1u;
+          const int src = ln[q] < 0 ? 0 : ln[q];
+          const int s = __shfl_sync(0xffffffffu, rec.x, src);
+          gq[q] = __int_as_float(__shfl_sync(0xffffffffu, rec.y, src));
+          const __nv_bfloat16* r = p.H + ((size_t)(b0 + src) * p.S + (s < 0 ? 0 : s)) * p.D + d0 + lane * 8;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            xq[q][c] = (ln[q] >= 0 && dvalid[c]) ? __ldg(reinterpret_cast<const int4*>(r + c * 256))
+                                                 : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < DES_U; ++q) {
+          if (ln[q] >= 0) {
+            gsum += gq[q];
+            const uint64_t gg = pack_gg(gq[q]);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) fma8(&acc[c * 8], gg, xq[q][c]);
+          }
+        }
+      }
+    }
+    OutT* dst = reinterpret_cast<OutT*>(p.dE) + (size_t)v * p.D + d0 + lane * 8;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (dvalid[c]) store8<OutT>(dst + c * 256, &acc[c * 8]);
+    if (blockIdx.y == 0 && lane == 0 && p.db != nullptr) p.db[v] = p.include_bias_grad ? gsum : 0.f;
+  }
 }
 
 // ------------------------------------------------------------------ K3a: route
@@ -597,7 +682,9 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
   const int n = min(RT_WIN, p.V - v0);
   const int seg_len = (n + nseg - 1) / nseg;
 
+  __shared__ unsigned int n_active;   // active pairs of this (b, window), for the sparse regime
   for (int i = threadIdx.x; i < nseg * S; i += RT_THREADS) hist[i] = 0;
+  if (threadIdx.x == 0) n_active = 0;
   __syncthreads();
 
   const float* Yb = p.Y + (size_t)b * p.ldY + v0;
@@ -613,6 +700,7 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
   int rk[RQ];
   float rg[RQ];
   int2* gib = p.gi ? p.gi + (size_t)b * p.ldGI + v0 : nullptr;
+  unsigned int nact = 0;
   if (gib != nullptr && w == nwin - 1 && threadIdx.x == 0)
     for (long long v = p.V; v < p.ldGI; ++v) p.gi[(size_t)b * p.ldGI + v] = make_int2(-1, 0);   // row padding
   if (warp < nseg) {
@@ -639,6 +727,7 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
           // (s, g) record for the staged dE; inactive pairs get s = -1 (a zero row).
           if (gib != nullptr && v < ve) gib[v] = make_int2(active ? k[q] : -1, __float_as_int(g));
           if (active) atomicAdd(&h[k[q]], 1);
+          nact += active;
           rk[q0 + q] = active ? k[q] : -1;
           rg[q0 + q] = g;
         }
@@ -655,11 +744,20 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (pair_active(y[q], k[q], S)) atomicAdd(&h[k[q]], 1);
+          if (pair_active(y[q], k[q], S)) {
+            atomicAdd(&h[k[q]], 1);
+            ++nact;
+          }
       }
     }
   }
+  if (p.stats != nullptr) {
+    nact = __reduce_add_sync(0xffffffffu, nact);
+    if (lane == 0 && nact) atomicAdd(&n_active, nact);
+  }
   __syncthreads();
+  if (p.stats != nullptr && threadIdx.x == 0 && n_active)
+    atomicAdd(p.stats, (unsigned long long)n_active);
 
   // Phase 2: exclusive scan over s of the per-s totals -> window-local list
   // offsets; then per-s exclusive scan over segments -> cursors (in hist).
@@ -763,7 +861,12 @@ sparton_bwd_route_kernel(const BwdParams p, int nseg, int nwin, int allow_stash)
 // each in ascending v, so the accumulation order is exactly the reference's
 // (v ascending, hidden_row / np.add.at).  Partial sums carry across launches in
 // fp32 (the output itself when it is fp32, else the workspace accumulator).
-template <int CPL, int DH_UNROLL, int MINB, bool FULL, typename OutT, int THREADS = DH_THREADS, bool FP8 = false>
+//
+// SPW (sparse regime, bf16 only): one launch walks the whole vocabulary in
+// groups of 32 windows without the fp32 carry (the few E rows it gathers need
+// no L2-sized chunks); the dense launches exit, or SPW exits when dense.
+template <int CPL, int DH_UNROLL, int MINB, bool FULL, typename OutT, int THREADS = DH_THREADS, bool FP8 = false,
+          bool SPW = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
   // Lane l owns columns d0 + c*256 + l*8 .. +8 of its row (bf16: one 16-B
@@ -773,16 +876,17 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long nrows = (long long)p.B * p.S;
+  if (!FP8 && p.stats != nullptr && dh_sparse(p) != SPW) return;
   // Persistent grid-stride over rows (b*S + s): one CTA per SM.
   for (long long rowid = (long long)blockIdx.x * (THREADS / 32) + warp; rowid < nrows;
        rowid += (long long)gridDim.x * (THREADS / 32)) {
   const int b = (int)(rowid / p.S);
   const int s = (int)(rowid - (long long)b * p.S);
   const int d0 = blockIdx.y * (256 * CPL);
-  const bool first = chunk == 0;
-  const bool last = chunk == p.nchunks - 1;
-  const int w0 = chunk * p.wpc;
-  const int w1 = min(p.nwin, w0 + p.wpc);
+  const bool first = SPW || chunk == 0;
+  const bool last = SPW || chunk == p.nchunks - 1;
+  const int w0 = SPW ? 0 : chunk * p.wpc;
+  const int w1 = SPW ? p.nwin : min(p.nwin, w0 + p.wpc);
 
   bool dvalid[CPL];
 #pragma unroll
@@ -811,14 +915,16 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
   }
 
   // The row's sub-lists of every window of this pass, read as one flattened
-  // list: lane t < nw fetches window w0+t's bounds (one round trip for all
+  // list: lane t < nw fetches window wg+t's bounds (one round trip for 32
   // windows), a prefix sum over lanes gives each window's start in the
   // flattened order, and each batch of 32 records is fetched in one load
   // (window order, then ascending v: the reference's summation order).
-  const int nw = w1 - w0;                  // <= 32 (wpc is capped on the host)
+  // Dense passes span <= 32 windows (wpc is capped on the host): one group.
+  for (int wg = w0; SPW ? wg < w1 : wg == w0; wg += 32) {
+  const int nw = SPW ? min(32, w1 - wg) : w1 - w0;
   int ks = 0, cnt = 0;
   if (lane < nw) {
-    const int* off = p.offsets + ((size_t)b * p.nwin + w0 + lane) * (p.S + 1);
+    const int* off = p.offsets + ((size_t)b * p.nwin + wg + lane) * (p.S + 1);
     ks = off[s];
     cnt = off[s + 1] - ks;
   }
@@ -830,7 +936,7 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   const int excl = incl - cnt;             // flattened start of window lane (lane < nw)
-  const int2* lst0 = p.pairs + (size_t)b * p.V + (size_t)w0 * RT_WIN;
+  const int2* lst0 = p.pairs + (size_t)b * p.V + (size_t)wg * RT_WIN;
   for (int base = 0; base < total; base += 32) {
     const int m = min(32, total - base);
     const int idx = base + lane;
@@ -878,6 +984,7 @@ sparton_bwd_dh_kernel(const BwdParams p, int chunk) {
       }
     }
   }
+  }  // window groups
 
   if (last) {
     if constexpr (FP8) {
@@ -1020,6 +1127,16 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return set_cuda_error("cudaDeviceGetAttribute(dh)", e);
   const dim3 grid(sms, dslices);
+  if constexpr (!FP8) {
+    if (p.stats != nullptr) {   // sparse-regime single pass (exits at once when dense)
+      if (full)
+        sparton_bwd_dh_kernel<CPL, 4, 1, true, OutT, DH_PERSIST_THREADS, false, true><<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, 0);
+      else
+        sparton_bwd_dh_kernel<CPL, 4, 1, false, OutT, DH_PERSIST_THREADS, false, true><<<grid, DH_PERSIST_THREADS, 0, stream>>>(p, 0);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel (sparse)", e);
+    }
+  }
   for (int c = 0; c < p.nchunks; ++c) {
     // FP8 rows are half as wide (8-B loads): 16 warps x 8 rows in flight.
     constexpr int T = FP8 ? DH_FP8_THREADS : DH_PERSIST_THREADS;
@@ -1031,6 +1148,24 @@ int launch_dh(const BwdParams& p, cudaStream_t stream) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_dh_kernel", e);
   }
+  return SPARTON_OK;
+}
+
+template <int CPL, typename OutT>
+int launch_de_sparse(const BwdParams& p, cudaStream_t stream) {
+  // One 512-thread CTA per SM, warps striding over vocab rows; the kernel
+  // exits at once unless the route counted a sparse batch.
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return set_cuda_error("cudaDeviceGetAttribute(de_sparse)", e);
+  const dim3 grid(sms, (p.D + 256 * CPL - 1) / (256 * CPL));
+  if (p.D % (256 * CPL) == 0)
+    sparton_bwd_de_sparse_kernel<CPL, true, OutT><<<grid, DES_THREADS, 0, stream>>>(p);
+  else
+    sparton_bwd_de_sparse_kernel<CPL, false, OutT><<<grid, DES_THREADS, 0, stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("launch sparton_bwd_de_sparse_kernel", e);
   return SPARTON_OK;
 }
 
@@ -1136,19 +1271,30 @@ int launch_bwd_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t stream
     return join();
   }
   if (p.gi != nullptr) {
-    // Staged dE needs the route's (s, g) records: route, then dE || dH.
+    // Staged dE needs the route's (s, g) records: route, then dE || dH.  The
+    // route also counts the active pairs; the staged dE + db and the sparse
+    // dE are both launched and exactly one of them runs (device-side choice).
+    if (p.stats != nullptr) {
+      e = cudaMemsetAsync(p.stats, 0, sizeof(unsigned long long), stream);
+      if (e != cudaSuccess) return set_cuda_error("zero the active-pair count", e);
+    }
     if ((rc = launch_route(p, stream)) != SPARTON_OK) return rc;
+    auto de = [&](cudaStream_t s) -> int {
+      int r = launch_de_staged<OutT>(p, tmH, s);
+      if (r == SPARTON_OK && p.stats != nullptr) r = launch_de_sparse<CPL, OutT>(p, s);
+      return r;
+    };
     if (mode == 0) {
-      if ((rc = launch_de_staged<OutT>(p, tmH, stream)) != SPARTON_OK) return rc;
+      if ((rc = de(stream)) != SPARTON_OK) return rc;
       if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
       return dh_done();
     }
     // Timing experiments only (tools/bwd_parts.py): one gradient family, the
     // others left unwritten (mode is only ever != 1 in a SPARTON_DEV=1 process).
     if (mode == 3 || mode == 4)
-      return mode == 3 ? launch_de_staged<OutT>(p, tmH, stream) : launch_dh<CPL, OutT>(p, stream);
+      return mode == 3 ? de(stream) : launch_dh<CPL, OutT>(p, stream);
     if ((rc = fork()) != SPARTON_OK) return rc;
-    if ((rc = launch_de_staged<OutT>(p, tmH, ss.s)) != SPARTON_OK) return rc;
+    if ((rc = de(ss.s)) != SPARTON_OK) return rc;
     if ((rc = launch_dh<CPL, OutT>(p, stream)) != SPARTON_OK) return rc;
     if ((rc = dh_done()) != SPARTON_OK) return rc;
     return join();
@@ -1231,7 +1377,8 @@ BwdWorkspace bwd_workspace_layout(long long B, long long S, long long D, long lo
   w.acc32 = w.dE_acc + (need_de_acc ? up((size_t)V * (size_t)D * sizeof(float)) : 0);
   const bool need_acc = grad_dtype == SPARTON_BF16 && w.nchunks > 1;
   w.gi = w.acc32 + (need_acc ? up((size_t)B * (size_t)S * (size_t)D * sizeof(float)) : 0);
-  w.total = w.gi + (w.de_staged ? up((size_t)B * (size_t)w.ldGI * sizeof(int2)) : 0);
+  w.stats = w.gi + (w.de_staged ? up((size_t)B * (size_t)w.ldGI * sizeof(int2)) : 0);
+  w.total = w.stats + 256;                   // active-pair count (sparse regime)
   if (!need_acc) w.acc32 = (size_t)-1;
   if (!need_de_acc) w.dE_acc = (size_t)-1;
   return w;

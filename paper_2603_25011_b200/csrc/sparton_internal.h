@@ -12,6 +12,9 @@
 namespace sparton {
 
 constexpr int kMaxFwdDst = 8;
+// Sparse-regime thresholds of the backward (percent of the B*V pairs active).
+constexpr double kDeSparsePct = 40.0;
+constexpr double kDhSparsePct = 12.0;
 
 struct FwdParams {
   const float* bias;
@@ -70,11 +73,20 @@ struct BwdParams {
   int fp8;
   const float* amax_h;
   const float* amax_e;
+  // Sparse regime (SPLADE representations: few active (b, v) pairs).  The
+  // route counts the active pairs into stats[0] (zeroed before it); with at
+  // most de_sparse_max active pairs dE runs as a per-pair gather (the staged
+  // dE and db kernels exit at once), with at most dh_sparse_max dH runs as one
+  // pass over the whole vocabulary without the fp32 carry.  Decided on the
+  // device: no host synchronisation.  stats == nullptr: dense kernels only.
+  unsigned long long* stats;
+  long long de_sparse_max;
+  long long dh_sparse_max;
 };
 
 // Workspace layout for sparton_bwd (byte offsets, 256-B aligned).
 struct BwdWorkspace {
-  size_t pairs, offsets, db_acc, dE_acc, acc32, gi, total;
+  size_t pairs, offsets, db_acc, dE_acc, acc32, gi, stats, total;
   long long ldGI;
   bool de_staged;
   int nwin, wpc, nchunks, bchunk;

@@ -48,15 +48,16 @@ def test_workspace_formula():
     # fp32 gradients carry dH partial sums in the output; bf16 needs an fp32 dH
     # carry because dH runs in vocab-chunk passes (cfg3: 384 MB of E).  The
     # staged dE keeps its sums in registers over the whole batch: no dE carry.
-    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_F32) == base + gi
-    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_BF16) == base + up(B * S * D * 4) + gi
+    st = 256                                     # active-pair count (sparse regime)
+    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_F32) == base + gi + st
+    assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_BF16) == base + up(B * S * D * 4) + gi + st
     # S beyond the staged dE's smem limit: gathered dE in batch-chunk passes with an fp32 carry
     S2 = 1024
     base2 = up(B * V * 8) + up(B * nwin * (S2 + 1) * 4) + up(V * 4)
-    assert lib.sparton_bwd_workspace_bytes(B, S2, D, V, _lib.SPARTON_BF16) == base2 + up(V * D * 4) + up(B * S2 * D * 4)
+    assert lib.sparton_bwd_workspace_bytes(B, S2, D, V, _lib.SPARTON_BF16) == base2 + up(V * D * 4) + up(B * S2 * D * 4) + st
     # a tiny problem is one window and one pass of each kind: no carry buffers
     assert lib.sparton_bwd_workspace_bytes(2, 3, 8, 5, _lib.SPARTON_BF16) == (
-        up(2 * 5 * 8) + up(2 * 1 * 4 * 4) + up(5 * 4) + up(2 * 6 * 8))
+        up(2 * 5 * 8) + up(2 * 1 * 4 * 4) + up(5 * 4) + up(2 * 6 * 8) + st)
     assert lib.sparton_bwd_workspace_bytes(0, S, D, V, 0) == 0
 
 
@@ -145,4 +146,4 @@ def test_staged_de_sequence_limit():
         base = up(B * V * 8) + up(B * nwin * (S + 1) * 4) + up(V * 4)
         extra = up(B * (V + V % 2) * 8) if staged else up(V * D * 4)
         assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_F32) == base + (
-            extra if staged else 0), S
+            extra if staged else 0) + 256, S
