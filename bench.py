@@ -65,18 +65,22 @@ def config_dict(cname, c, world):
                 c["B"] * c["S"] * c["D"] * 2 >> 20, c["V"] * c["D"] * 2 >> 20, c["B"] * c["V"] * 4 >> 20)}
 
 
+SPARSE_BIAS = -2.0   # SURVEY §8d "SPLADE-sparse" variant
 DH_CHUNK_MB = 52   # csrc/sparton_bwd.cu DH_CHUNK_BYTES (tests/test_host.py keeps them equal)
 
 
 def launches_per_step(c, v_local):
     """Kernels the library launches per step (fwd + bwd) on one rank:
-    K1 + route + staged dE + db column sum + one dH launch per L2-sized
-    vocabulary chunk (csrc/sparton_bwd.cu: RT_WIN = 8192 rows per route
-    window, DH_CHUNK_BYTES of E per chunk)."""
+    K1 + route + staged dE + db column sum + sparse dE + single-pass dH + one
+    dH launch per L2-sized vocabulary chunk (csrc/sparton_bwd.cu: RT_WIN =
+    8192 rows per route window, DH_CHUNK_BYTES of E per chunk).  The
+    sparse-regime pair (and, in that regime, the staged dE, db and dense dH
+    launches) exit on their first instruction after reading the route's
+    active-pair count; all are launched."""
     D = c["D"]
     nwin = -(-v_local // 8192)
     wpc = max(1, min(nwin, 32, (DH_CHUNK_MB << 20) // (8192 * D * 2)))
-    return 1 + 1 + 1 + 1 + -(-nwin // wpc)
+    return 1 + 1 + 1 + 1 + 2 + -(-nwin // wpc)
 
 
 def measured_peaks():
@@ -267,7 +271,7 @@ def run_reference_arm(args, c, cname):
 
 # ---------------------------------------------------------------- GPU arm
 
-def make_inputs(c, dev, rank, world):
+def make_inputs(c, dev, rank, world, bias_value=0.0):
     import torch
     gen = torch.Generator(device=dev).manual_seed(0)
     B, S, D, V = c["B"], c["S"], c["D"], c["V"]
@@ -284,7 +288,7 @@ def make_inputs(c, dev, rank, world):
         lo, hi = max(r0, v0), min(r1, v1)
         if lo < hi:
             E_rows[lo - v0:hi - v0] = x[lo - r0:hi - r0]
-    bias = torch.zeros(v1 - v0, device=dev)
+    bias = torch.full((v1 - v0,), float(bias_value), device=dev)
     mask = torch.ones((B, S), dtype=torch.uint8, device=dev)
     g3 = torch.Generator(device=dev).manual_seed(2)
     dY = torch.randn((B, V), generator=g3, device=dev)
@@ -302,7 +306,7 @@ def _max_over_ranks(vals, world, dev):
     return [float(x) for x in t]
 
 
-def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False):
+def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False, bias_value=0.0):
     """Warm up, then time `steps` fwd+bwd steps between barriers; returns
     (ms per step, mean forward ms, peak bytes, head-owned peak bytes, inputs).
     ``fused``: N > 1 with the (Y, I) all-gather fused into K1's epilogue
@@ -312,7 +316,7 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False):
     from paper_2603_25011_b200 import sharded, sparton_backward, sparton_forward
 
     V = c["V"]
-    H, E, bias, mask, dY, (v0, v1, Vp) = make_inputs(c, dev, rank, world)
+    H, E, bias, mask, dY, (v0, v1, Vp) = make_inputs(c, dev, rank, world, bias_value)
     stream = torch.cuda.current_stream()
     fwd_ev = [] if fwd_ev is None else fwd_ev
     fg = sharded.FusedVocabGather.symmetric(c["B"], V, dev) if fused else None
@@ -439,6 +443,23 @@ def run_gpu_arm(args, c, cname):
         except Exception as exc:
             line["fused_gather"] = {"unavailable": repr(exc)[:300]}
         torch.cuda.empty_cache()
+    if world == 1 and not args.no_sparse:
+        # SURVEY §8d secondary run: the SPLADE-sparse variant (bias -2: a few %
+        # of the (b, v) pairs active, as in trained SPLADE heads), where the
+        # backward takes its sparse-regime kernels.
+        sev = []
+        mss, fws, _, _, inps = timed_steps(c, dev, rank, world, args.steps, args.warmup, sev, bias_value=SPARSE_BIAS)
+        Hs, Es, bs, ms_, _, _ = inps
+        from paper_2603_25011_b200 import sparton_forward
+        Ys, _ = sparton_forward(Hs, Es, bs, ms_)
+        act = float((Ys > 0).float().mean())
+        del inps, Hs, Es, bs, ms_, Ys
+        torch.cuda.empty_cache()
+        line["splade_sparse"] = {"bias": SPARSE_BIAS, "active_pair_fraction": act, "ms_per_step": mss,
+                                 "fwd_ms": fws, "bwd_ms": mss - fws, "steps": args.steps,
+                                 "value": (ff + fb) / (mss * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                 "note": "same workload with bias -2 (few % active pairs): the backward "
+                                         "runs its sparse-regime kernels (per-pair dE gathers, single-pass dH)"}
     if world > 1 and not args.no_cfg4:
         c4 = CONFIGS["cfg4"]
         ms4, fwd4, peak4, _, inp4 = timed_steps(c4, dev, rank, world, args.steps, args.warmup)
@@ -598,6 +619,7 @@ def main() -> int:
     ap.add_argument("--no-plugin", action="store_true", help="skip the numpy drop-in e2e record")
     ap.add_argument("--no-cfg4", action="store_true", help="N>1: skip the cfg4 record")
     ap.add_argument("--no-fused-ab", action="store_true", help="N>1: skip the fused all-gather A/B record")
+    ap.add_argument("--no-sparse", action="store_true", help="N=1: skip the SPLADE-sparse (bias -2) record")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":

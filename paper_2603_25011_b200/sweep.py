@@ -7,7 +7,9 @@ one row per axis value, timed on the device, OOM rows kept with ``OOM``
 sentinels.  The reference columns keep their meaning — ``peak_bytes`` is the
 torch allocator's peak over the timed calls, ``saved_bytes`` the (Y, I) state
 kept for backward, ``y_checksum`` the CRC32 of Y — and GPU columns are
-appended: the forward and fwd+bwd medians and the algorithmic TFLOP/s.
+appended: the forward and fwd+bwd medians, the algorithmic TFLOP/s, and the
+cost model's compulsory bytes of the b200 plan (``costmodel.b200_traffic``:
+forward, backward) with the forward's model bytes over its median time.
 
     python -m paper_2603_25011_b200.sweep --base 512,512,768,30522 --axis V \
         --values 30522,250002 --out sweep.csv
@@ -27,7 +29,7 @@ from .head import sparton_backward, sparton_forward
 
 REFERENCE_HEADER = ("strategy,B,S,D,V,vocab_tile,batch_tile,threads,"
                     "time_ms_med,time_ms_p10,time_ms_p90,peak_bytes,saved_bytes,y_checksum")
-GPU_COLUMNS = "fwd_ms_med,fwdbwd_ms_med,fwdbwd_tflops"
+GPU_COLUMNS = "fwd_ms_med,fwdbwd_ms_med,fwdbwd_tflops,fwd_model_bytes,bwd_model_bytes,fwd_model_gbs"
 HEADER = REFERENCE_HEADER + "," + GPU_COLUMNS
 AXES = ("B", "S", "D", "V")
 
@@ -76,11 +78,22 @@ def sweep_point(B: int, S: int, D: int, V: int, *, repeats: int = 5, warmup: int
         ck = y_checksum(Y.cpu().numpy())
         flops = 2 * B * S * V * D + 4 * B * V * D
         med = statistics.median(fwd)
+        fb, bb = _model_bytes(B, S, D, V)
         return (f"b200,{B},{S},{D},{V},{128 * 2},{1},{1},{med:.6g},{_pct(fwd, 10):.6g},{_pct(fwd, 90):.6g},"
                 f"{peak},{saved},{ck},{med:.6g},{statistics.median(both):.6g},"
-                f"{flops / (statistics.median(both) * 1e-3) / 1e12:.6g}")
+                f"{flops / (statistics.median(both) * 1e-3) / 1e12:.6g},{fb},{bb},{fb / (med * 1e-3) / 1e9:.6g}")
     except torch.OutOfMemoryError:
-        return f"b200,{B},{S},{D},{V},256,1,1,OOM,OOM,OOM,OOM,OOM,OOM,OOM,OOM,OOM"
+        fb, bb = _model_bytes(B, S, D, V)
+        return f"b200,{B},{S},{D},{V},256,1,1,OOM,OOM,OOM,OOM,OOM,OOM,OOM,OOM,OOM,{fb},{bb},OOM"
+
+
+def _model_bytes(B, S, D, V):
+    """(forward, backward) compulsory bytes of the b200 plan (costmodel.py)."""
+    from . import costmodel
+    from .fusedhead import Dims
+    rep = costmodel.b200_traffic(Dims(B, S, D, V))
+    st = rep.stages
+    return st[0].bytes_read + st[0].bytes_written, sum(x.bytes_read + x.bytes_written for x in st[1:])
 
 
 def run_sweep(base: tuple[int, int, int, int], axis: str, values, **kw) -> list[str]:

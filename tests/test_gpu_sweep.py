@@ -19,3 +19,5 @@ def test_sweep_rows(cuda_device):
         assert len(f) == ncol and f[0] == "b200" and int(f[4]) == v
         assert float(f[8]) > 0 and int(f[12]) == 2 * v * 8     # saved (Y, I) bytes = B*V*8
         assert len(f[13]) == 8
+        assert int(f[17]) == 2 * 40 * 64 * 2 + v * 64 * 2 + v * 4 + 2 * 40 + 2 * v * 8   # model fwd bytes
+        assert int(f[18]) > 0 and float(f[19]) > 0

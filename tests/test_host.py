@@ -116,5 +116,32 @@ def test_bench_launch_count_matches_library_constants():
     win = int(re.search(r"constexpr int RT_WIN = (\d+);", src).group(1))
     assert bench.DH_CHUNK_MB == chunk and win == 8192
     cfg3 = {"D": 768}
-    assert bench.launches_per_step(cfg3, 250002) == 4 + 8     # 31 windows, 4 per 52 MB pass
-    assert bench.launches_per_step(cfg3, 30522) == 4 + 1
+    assert bench.launches_per_step(cfg3, 250002) == 6 + 8     # 31 windows, 4 per 52 MB pass
+    assert bench.launches_per_step(cfg3, 30522) == 6 + 1
+
+
+def test_cost_model_b200_plan():
+    """costmodel.b200_traffic: the forward's compulsory bytes (H + E + bias +
+    mask in, Y + I out; 1.812 GB at cfg3), its peak equal to
+    the library's workspace query, and the reference's CSV schema."""
+    import io
+    import contextlib
+    from paper_2603_25011_b200 import _lib, costmodel as cm
+    from paper_2603_25011_b200.fusedhead import Dims
+    rep = cm.b200_traffic(Dims(512, 512, 768, 250002))
+    fwd = rep.stages[0]
+    assert fwd.label == "k1-fwd" and abs((fwd.bytes_read + fwd.bytes_written) / 1e9 - 1.812) < 0.001
+    assert rep.saved_state_bytes == 512 * 250002 * 8
+    lib = _lib.load()
+    for dims in [(512, 512, 768, 250002), (512, 1024, 768, 250002), (2, 3, 8, 5), (4, 300, 256, 1000),
+                 (2048, 512, 1024, 250002)]:
+        for gd, gb in ((_lib.SPARTON_F32, 4), (_lib.SPARTON_BF16, 2)):
+            assert lib.sparton_bwd_workspace_bytes(*dims, gd) == cm.workspace_bytes(*dims, gb), dims
+    rows = cm._cm.reports_to_csv_rows(cm.all_reports(Dims(8, 128, 768, 30522)))
+    b200 = [r for r in rows if r.startswith("b200,")]
+    assert [r.split(",")[1] for r in b200] == ["k1-fwd", "bwd-route", "bwd-dE", "bwd-dH", "total"]
+    assert all(len(r.split(",")) == len(cm.COST_CSV_HEADER.split(",")) for r in rows)
+    out = io.StringIO()
+    with contextlib.redirect_stdout(out):
+        assert cm.main(["--dims", "8x128x768x30522"]) == 0
+    assert "b200" in out.getvalue() and "fully_fused" in out.getvalue()
