@@ -115,6 +115,29 @@ SPARTON_API int sparton_fwd_multi(const void* H, const void* E, const float* bia
  * aligned): amax (device f32 scalar) = max |x|, q = e4m3(x * 448 / amax). */
 SPARTON_API int sparton_quantize_e4m3(const void* x_bf16, int64_t n, void* q_e4m3, float* amax, void* stream);
 
+/*
+ * MXFP8 forward (tcgen05 block-scaled MXFP8): e4m3
+ * operands with one ue8m0 scale per 32 consecutive K elements of every row
+ * (OCP MX), applied inside the MMA (tcgen05.mma kind::mxf8f6f4.block_scale,
+ * scales staged smem -> TMEM by tcgen05.cp).  Hq/Eq and Hsf/Esf come from
+ * sparton_quantize_mx; logit = sum_k 2^(sh-127) qh * 2^(se-127) qe + bias.
+ * Sequence chunks are 240 positions (TMEM columns 240..255 hold the scale
+ * factors).  D a multiple of 16; otherwise identical to sparton_fwd.
+ * Replaces no reference function (the paper's future work).
+ */
+enum { SPARTON_MX_H = 0, SPARTON_MX_E = 1 };
+/* Bytes of the scale-factor buffer of operand H (B, S, D) or E (V, D). */
+SPARTON_API int64_t sparton_mx_scales_bytes(int64_t B, int64_t S, int64_t D, int64_t V, int operand);
+/* Quantise bf16 x (H as B*S x D, or E as V x D) to e4m3 q (same shape) and
+ * ue8m0 scales sf (sf_bytes >= sparton_mx_scales_bytes), in the layout the
+ * forward's stages load: 2^e per 32-element block, the smallest power of two
+ * with max|x|/2^e <= 448, q = e4m3_rn(x / 2^e). */
+SPARTON_API int sparton_quantize_mx(const void* x_bf16, int64_t B, int64_t S, int64_t D, int64_t V, int operand,
+                                    void* q_e4m3, void* sf, size_t sf_bytes, void* stream);
+SPARTON_API int sparton_fwd_mx(const void* Hq, const void* Hsf, const void* Eq, const void* Esf,
+                               const float* bias, const uint8_t* mask, float* Y, int32_t* I,
+                               int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, void* stream);
+
 /* Workspace bytes sparton_bwd needs for these sizes: the argmax-routed (v, g)
  * pair lists for dH (B*V*8 bytes) and their offsets, the per-(b, v) (s, g)
  * records of the staged dE (B*V*8 bytes, S <= 832), plus an fp32 dH

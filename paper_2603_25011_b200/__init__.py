@@ -11,9 +11,10 @@ Public surface:
   * vocab-sharded multi-GPU head: ``paper_2603_25011_b200.sharded``
 """
 
-from .head import (SpartonHeadFn, SpartonHeadFp8Fn, bwd_workspace_bytes, quantize_e4m3, sparton_backward,
-                   sparton_backward_fp8, sparton_backward_fp32, sparton_forward, sparton_forward_fp8,
-                   sparton_forward_fp32, sparton_head, sparton_head_fp8, split_bf16x3)
+from .head import (SpartonHeadFn, SpartonHeadFp8Fn, bwd_workspace_bytes, dequantize_mx, quantize_e4m3, quantize_mx,
+                   sparton_backward, sparton_backward_fp8, sparton_backward_fp32, sparton_forward,
+                   sparton_forward_fp8, sparton_forward_fp32, sparton_forward_mx, sparton_head, sparton_head_fp8,
+                   split_bf16x3)
 
 __version__ = "0.1.0"
 
@@ -30,5 +31,8 @@ __all__ = [
     "split_bf16x3",
     "sparton_forward_fp8",
     "quantize_e4m3",
+    "sparton_forward_mx",
+    "quantize_mx",
+    "dequantize_mx",
     "sparton_head",
 ]

@@ -31,6 +31,8 @@ SPARTON_ECUDA = 2
 SPARTON_ENOTSUP = 3
 SPARTON_F32 = 0
 SPARTON_BF16 = 1
+SPARTON_MX_H = 0
+SPARTON_MX_E = 1
 
 # Every entry point include/sparton.h declares (checked by tests/test_abi.py).
 EXPORTED = (
@@ -45,6 +47,9 @@ EXPORTED = (
     "sparton_bwd",
     "sparton_bwd_ex",
     "sparton_bwd_fp8",
+    "sparton_mx_scales_bytes",
+    "sparton_quantize_mx",
+    "sparton_fwd_mx",
 )
 
 _lock = threading.Lock()
@@ -94,6 +99,12 @@ def load() -> ctypes.CDLL:
                                     c_int, c_int, c_vp, ctypes.c_size_t, c_vp]
         lib.sparton_bwd_ex.restype = c_int
         lib.sparton_bwd_ex.argtypes = lib.sparton_bwd.argtypes + [c_vp]
+        lib.sparton_mx_scales_bytes.restype = c_i64
+        lib.sparton_mx_scales_bytes.argtypes = [c_i64, c_i64, c_i64, c_i64, c_int]
+        lib.sparton_quantize_mx.restype = c_int
+        lib.sparton_quantize_mx.argtypes = [c_vp, c_i64, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, ctypes.c_size_t, c_vp]
+        lib.sparton_fwd_mx.restype = c_int
+        lib.sparton_fwd_mx.argtypes = [c_vp] * 8 + [c_i64] * 5 + [c_vp]
         lib.sparton_bwd_fp8.restype = c_int
         lib.sparton_bwd_fp8.argtypes = [c_vp] * 10 + [c_i64] * 6 + [c_int, c_int, c_vp, ctypes.c_size_t, c_vp, c_vp]
         _lib = lib

@@ -271,6 +271,57 @@ __device__ __forceinline__ void umma_e4m3(uint32_t tmem_d, uint64_t da, uint64_t
   }
 }
 
+// Instruction descriptor, kind::mxf8f6f4.block_scale: e4m3 x e4m3 -> f32 with
+// ue8m0 scale factors (one per 32 K elements, scale_vec::1X), both K-major.
+// Block-scaled layout: [4,6) B scale-factor id, [7,10)/[10,13) A/B format
+// (0 = E4M3), [17,23) N>>3, [23] scale format (1 = UE8M0), [24,29) M>>4,
+// [29,31) A scale-factor id.  The ids select the byte of the 32-bit TMEM
+// scale column: the K block (0..3) of a 128-element stage.
+__host__ __device__ constexpr uint32_t umma_idesc_mx(int M, int N) {
+  return ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t umma_idesc_mx_sf(uint32_t idesc, int kblk) {
+  return idesc | ((uint32_t)kblk << 4) | ((uint32_t)kblk << 29);
+}
+
+template <int CG>
+__device__ __forceinline__ void umma_mx(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t tsfa, uint32_t tsfb, uint32_t accumulate) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
+        :: "r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(tsfa), "r"(tsfb) : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
+        :: "r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(tsfa), "r"(tsfb) : "memory");
+  }
+}
+
+// Shared-memory descriptor of a no-swizzle K-major matrix of 16-byte rows
+// (core matrices of 8 rows x 16 B, 128 B apart): the source of tcgen05.cp.
+__device__ __forceinline__ uint64_t smem_desc_rows16(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128 >> 4) << 16;        // LBO
+  d |= (uint64_t)(128 >> 4) << 32;        // SBO: next 8-row core matrix
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  return d;                               // layout type 0: no swizzle
+}
+
+// smem -> TMEM: 32 rows x 128 bits, replicated to the four 32-lane quarters
+// (row r lands in lanes r, r+32, r+64, r+96; its 16 bytes in 4 columns).
+// CG==2: issued by the pair leader, each CTA copies its own smem to its TMEM.
+template <int CG>
+__device__ __forceinline__ void utccp_32x128b_x4(uint32_t taddr, uint64_t sdesc) {
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" :: "r"(taddr), "l"(sdesc) : "memory");
+  else
+    asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" :: "r"(taddr), "l"(sdesc) : "memory");
+}
+
 template <int CG>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                           uint32_t accumulate) {

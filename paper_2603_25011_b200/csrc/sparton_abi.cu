@@ -84,6 +84,25 @@ int encode_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols,
   return SPARTON_OK;
 }
 
+// Rows of `cols` uint32 (scale-factor chunks), boxes of box_rows rows.
+int encode_2d_u32(CUtensorMap* map, const void* ptr, long long rows, int cols, int box_rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return set_error(SPARTON_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (scale factors) failed (CUresult %d) rows=%lld", (int)r, rows);
+    return set_error(SPARTON_ECUDA, buf);
+  }
+  return SPARTON_OK;
+}
+
 int encode_bf16_2d_swz(CUtensorMap* map, const void* ptr, long long rows, long long cols,
                        int box_rows, int box_cols, CUtensorMapSwizzle swz) {
   return encode_2d(map, ptr, rows, cols, box_rows, box_cols, swz, false);
@@ -173,17 +192,25 @@ static int check_device() {
   return SPARTON_OK;
 }
 
+// fp8: 0 bf16 operands, 1 e4m3 with per-tensor amax scales, 2 MXFP8 (e4m3
+// with the ue8m0 block scales Hsf / Esf of sparton_quantize_mx_{h,e}).
 static int fwd_common(const void* H, const void* E, const float* amax_h, const float* amax_e, const float* bias,
                       const uint8_t* mask, float* Y, int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V,
-                      int64_t ldY, int cta_group, void* stream, bool fp8, int nx = 0,
-                      float* const* Yx = nullptr, int32_t* const* Ix = nullptr) {
+                      int64_t ldY, int cta_group, void* stream, int fp8, int nx = 0,
+                      float* const* Yx = nullptr, int32_t* const* Ix = nullptr, const void* Hsf = nullptr,
+                      const void* Esf = nullptr) {
   int rc = check_dims(B, S, D, V);
   if (rc) return rc;
   if (!H || !E || !bias || !mask || !Y || !I) return set_error(SPARTON_EINVAL, "null pointer argument");
   if (nx < 0 || nx > kMaxFwdDst - 1) return set_error(SPARTON_EINVAL, "ndst must lie in [1, 8]");
   for (int k = 0; k < nx; ++k)
     if (!Yx[k] || !Ix[k]) return set_error(SPARTON_EINVAL, "null destination pointer");
-  if (fp8 && (!amax_h || !amax_e)) return set_error(SPARTON_EINVAL, "null amax pointer");
+  if (fp8 == 1 && (!amax_h || !amax_e)) return set_error(SPARTON_EINVAL, "null amax pointer");
+  if (fp8 == 2 && (!Hsf || !Esf)) return set_error(SPARTON_EINVAL, "null scale-factor pointer");
+  if (fp8 == 2 && cta_group != 0 && cta_group != 2)
+    return set_error(SPARTON_EINVAL, "MXFP8 runs on CTA pairs (cta_group 0 or 2)");
+  if (fp8 == 2 && (!aligned16(Hsf) || !aligned16(Esf)))
+    return set_error(SPARTON_EINVAL, "scale factors must be 16-byte aligned");
   if (fp8 && D % 16 != 0)
     return set_error(SPARTON_EINVAL, "e4m3 operands need D to be a multiple of 16 (TMA 16-byte stride)");
   if (!aligned16(H) || !aligned16(E)) return set_error(SPARTON_EINVAL, "H and E must be 16-byte aligned");
@@ -201,12 +228,19 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
     cg = 2;
     if (const char* ev = dev_env("SPARTON_FWD_CLUSTER")) cg = atoi(ev);
     if (cg != 1 && cg != 2 && cg != 4) cg = 2;
+    if (fp8 == 2) cg = 2;
   }
   // One 128-byte swizzle row per K step: 64 bf16 or 128 e4m3 columns.
   const int box_cols = fp8 ? 128 : 64;
   CUtensorMap tmE, tmH;
   if ((rc = encode_2d(&tmE, E, V, D, 128, box_cols, CU_TENSOR_MAP_SWIZZLE_128B, fp8))) return rc;
-  if ((rc = encode_2d(&tmH, H, B * S, D, fwd_h_box_rows(cg), box_cols, CU_TENSOR_MAP_SWIZZLE_128B, fp8))) return rc;
+  if ((rc = encode_2d(&tmH, H, B * S, D, fwd_h_box_rows(cg, fp8), box_cols, CU_TENSOR_MAP_SWIZZLE_128B, fp8))) return rc;
+  // MX scale factors as rows of 128 uint32 (one 512-B chunk per row).
+  CUtensorMap tmSFA, tmSFB;
+  if (fp8 == 2) {
+    const long long ra = mx_sf_bytes(false, V, 1, (int)D) / 512, rb = mx_sf_bytes(true, B, S, (int)D) / 512;
+    if ((rc = encode_2d_u32(&tmSFA, Esf, ra, 128, 1)) || (rc = encode_2d_u32(&tmSFB, Hsf, rb, 128, 2))) return rc;
+  }
   FwdParams prm = {};
   prm.bias = bias;
   prm.mask = mask;
@@ -217,7 +251,7 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
   prm.D = (int)D;
   prm.V = (int)V;
   prm.ldY = ldY;
-  prm.fp8 = fp8 ? 1 : 0;
+  prm.fp8 = fp8;
   prm.nx = nx;
   for (int k = 0; k < nx; ++k) {
     prm.Yx[k] = Yx[k];
@@ -231,13 +265,14 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
     // Both evict_last measured lowest DRAM traffic (profiles/r01_fwd_l2_policy.txt).
     prm.e_evict_last = ev ? atoi(ev) : 5;
   }
-  return launch_fwd(tmE, tmH, prm, cg, d.sms, static_cast<cudaStream_t>(stream));
+  return launch_fwd(tmE, tmH, fp8 == 2 ? &tmSFA : nullptr, fp8 == 2 ? &tmSFB : nullptr, prm, cg, d.sms,
+                    static_cast<cudaStream_t>(stream));
 }
 
 int sparton_fwd(const void* H, const void* E, const float* bias, const uint8_t* mask, float* Y,
                 int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int cta_group,
                 void* stream) {
-  return fwd_common(H, E, nullptr, nullptr, bias, mask, Y, I, B, S, D, V, ldY, cta_group, stream, false);
+  return fwd_common(H, E, nullptr, nullptr, bias, mask, Y, I, B, S, D, V, ldY, cta_group, stream, 0);
 }
 
 int sparton_fwd_multi(const void* H, const void* E, const float* bias, const uint8_t* mask, int ndst,
@@ -246,13 +281,43 @@ int sparton_fwd_multi(const void* H, const void* E, const float* bias, const uin
   if (ndst < 1 || ndst > kMaxFwdDst || !Y_dst || !I_dst)
     return set_error(SPARTON_EINVAL, "ndst must lie in [1, 8] with non-null destination arrays");
   return fwd_common(H, E, nullptr, nullptr, bias, mask, Y_dst[0], I_dst[0], B, S, D, V, ldY, cta_group, stream,
-                    false, ndst - 1, Y_dst + 1, I_dst + 1);
+                    0, ndst - 1, Y_dst + 1, I_dst + 1);
 }
 
 int sparton_fwd_fp8(const void* H8, const void* E8, const float* amax_h, const float* amax_e, const float* bias,
                     const uint8_t* mask, float* Y, int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V,
                     int64_t ldY, int cta_group, void* stream) {
-  return fwd_common(H8, E8, amax_h, amax_e, bias, mask, Y, I, B, S, D, V, ldY, cta_group, stream, true);
+  return fwd_common(H8, E8, amax_h, amax_e, bias, mask, Y, I, B, S, D, V, ldY, cta_group, stream, 1);
+}
+
+int64_t sparton_mx_scales_bytes(int64_t B, int64_t S, int64_t D, int64_t V, int operand) {
+  if (B < 1 || S < 1 || D < 1 || V < 1 || (operand != SPARTON_MX_H && operand != SPARTON_MX_E)) return 0;
+  return operand == SPARTON_MX_H ? mx_sf_bytes(true, B, S, (int)D) : mx_sf_bytes(false, V, 1, (int)D);
+}
+
+int sparton_quantize_mx(const void* x, int64_t B, int64_t S, int64_t D, int64_t V, int operand, void* q, void* sf,
+                        size_t sf_bytes, void* stream) {
+  int rc = check_dims(B, S, D, V);
+  if (rc) return rc;
+  if (operand != SPARTON_MX_H && operand != SPARTON_MX_E)
+    return set_error(SPARTON_EINVAL, "operand must be SPARTON_MX_H or SPARTON_MX_E");
+  if (!x || !q || !sf) return set_error(SPARTON_EINVAL, "null pointer argument");
+  if (D % 16 != 0) return set_error(SPARTON_EINVAL, "e4m3 operands need D to be a multiple of 16");
+  if (!aligned16(x) || !aligned16(q) || !aligned16(sf))
+    return set_error(SPARTON_EINVAL, "x, q and sf must be 16-byte aligned");
+  if ((int64_t)sf_bytes < sparton_mx_scales_bytes(B, S, D, V, operand))
+    return set_error(SPARTON_EINVAL, "scale-factor buffer too small (sparton_mx_scales_bytes)");
+  if ((rc = check_device())) return rc;
+  const bool h = operand == SPARTON_MX_H;
+  return launch_quantize_mx(h, x, h ? B : V, h ? S : 1, (int)D, q, sf, static_cast<cudaStream_t>(stream));
+}
+
+int sparton_fwd_mx(const void* Hq, const void* Hsf, const void* Eq, const void* Esf, const float* bias,
+                   const uint8_t* mask, float* Y, int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V,
+                   int64_t ldY, void* stream) {
+  if (D % 16 != 0) return set_error(SPARTON_EINVAL, "e4m3 operands need D to be a multiple of 16");
+  return fwd_common(Hq, Eq, nullptr, nullptr, bias, mask, Y, I, B, S, D, V, ldY, 0, stream, 2, 0, nullptr, nullptr,
+                    Hsf, Esf);
 }
 
 int sparton_quantize_e4m3(const void* x, int64_t n, void* q, float* amax, void* stream) {

@@ -36,19 +36,32 @@
 
 namespace sparton {
 
-template <int CG, int NP = 1, bool FP8 = false>
+// OP: operand format — 0 bf16, 1 e4m3 with per-tensor scales (kind::f8f6f4),
+// 2 MXFP8: e4m3 with a ue8m0 scale per 32 K elements of every row, applied
+// inside the MMA (kind::mxf8f6f4.block_scale, scale factors in TMEM).
+template <int CG, int NP = 1, int OP = 0>
 struct FwdCfg {
+  static constexpr bool FP8 = OP != 0;           // e4m3 operands
+  static constexpr bool MX = OP == 2;            // block-scaled (MXFP8)
   static constexpr int EB = FP8 ? 1 : 2;         // operand element bytes (e4m3 / bf16)
   static constexpr int BM = 128;                 // vocab rows per CTA (TMEM lanes)
   static constexpr int TILE_V = BM * CG * NP;    // vocab rows per unit (NP pairs share H tiles)
-  static constexpr int SN = 256;                 // sequence positions per chunk (UMMA N)
+  // Sequence positions per chunk (UMMA N).  MX: 240, so columns 240..255 of
+  // the first accumulator hold the stage's scale factors (TMEM is otherwise
+  // fully taken by the two 256-column accumulators).
+  static constexpr int SN = MX ? 240 : 256;
   static constexpr int BN_CTA = SN / CG;         // H rows each CTA holds per chunk
   static constexpr int BN_LOAD = BN_CTA / NP;    // H rows each CTA loads (and multicasts to NP CTAs)
   static constexpr int BK = 128 / EB;            // K per stage = one 128-B swizzle row
   static constexpr int KSTEPS = 4;               // UMMA K = 16 (bf16) / 32 (e4m3): 32 B per step
   static constexpr int A_BYTES = BM * BK * EB;
   static constexpr int B_BYTES = BN_CTA * BK * EB;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // MX scale factors per stage (4 K blocks of 32): this CTA's 128 E rows
+  // (512 B) and the chunk's 256 H-row slots (1 KB), in the tcgen05.cp layout.
+  static constexpr int SF_BYTES = MX ? 3 * 512 : 0;
+  static constexpr int STAGE_TX = A_BYTES + B_BYTES + SF_BYTES;   // bytes landing per stage
+  static constexpr int STAGE_BYTES = (STAGE_TX + 1023) / 1024 * 1024;
+  static constexpr int SF_COL = 240;             // MX: TMEM column of SFA (4 cols), SFB follows (8 cols)
   static constexpr int NST = CG == 1 ? 4 : 6;   // 7 stages measured 0.8% slower (tools/ab_fwd.sh)
   static constexpr int UMMA_M = BM * CG;
   static constexpr int NUM_THREADS = 192;
@@ -189,11 +202,14 @@ __device__ __forceinline__ void store_yi(const FwdParams& p, size_t o, float y, 
   }
 }
 
-template <int CG, int NP, bool FP8>
-__global__ void __launch_bounds__(FwdCfg<CG, NP, FP8>::NUM_THREADS, 1)
+template <int CG, int NP, int OP>
+__global__ void __launch_bounds__(FwdCfg<CG, NP, OP>::NUM_THREADS, 1)
 sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmH,
+                   const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                    const FwdParams p) {
-  using C = FwdCfg<CG, NP, FP8>;
+  using C = FwdCfg<CG, NP, OP>;
+  constexpr bool FP8 = C::FP8;
+  static_assert(!C::MX || (CG == 2 && NP == 1), "MXFP8 runs on the CTA-pair kernel");
   static_assert(NP == 1 || CG == 2, "H multicast across pairs needs CTA pairs");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128-B swizzle atoms.
@@ -224,6 +240,10 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
   if (warp == kProducer && lane == 0) {
     ptx::prefetch_tmap(&tmE);
     ptx::prefetch_tmap(&tmH);
+    if constexpr (C::MX) {
+      ptx::prefetch_tmap(&tmSFA);
+      ptx::prefetch_tmap(&tmSFB);
+    }
     for (int i = 0; i < C::NST; ++i) {
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&empty[i]), NP);   // one MMA commit per pair (multicast H)
@@ -273,12 +293,20 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
             const uint32_t sb = sa + C::A_BYTES;
             const uint32_t fb = ptx::smem_u32(&full[st]);
             if constexpr (CG == 1) {
-              ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+              ptx::mbar_arrive_expect_tx(fb, C::STAGE_TX);
               ptx::tma_load_2d(&tmE, sa, fb, kb * C::BK, vrow, pol_e);
               ptx::tma_load_2d(&tmH, sb, fb, kb * C::BK, hrow, pol_h);
             } else {
-              if (rank == 0) ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES * 2);
+              if (rank == 0) ptx::mbar_arrive_expect_tx(fb, C::STAGE_TX * 2);
               ptx::tma_load_2d_cg2(&tmE, sa, fb, kb * C::BK, vrow, pol_e);
+              if constexpr (C::MX) {
+                // Scale factors (uint32 rows of 128 = one 512-B chunk): this
+                // CTA's E rows (vrow / 128, K group kb) and the chunk's H slot
+                // pair ((unit row, chunk), K group kb) — see sparton_quant_mx.
+                const uint32_t ssf = sb + C::B_BYTES;
+                ptx::tma_load_2d_cg2(&tmSFA, ssf, fb, 0, (vrow >> 7) * nkb + kb, pol_e);
+                ptx::tma_load_2d_cg2(&tmSFB, ssf + 512, fb, 0, ((b * nsc + sc) * nkb + kb) * 2, pol_h);
+              }
               if constexpr (NP == 1) {
                 ptx::tma_load_2d_cg2(&tmH, sb, fb, kb * C::BK, hrow, pol_h);
               } else {
@@ -299,11 +327,14 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     if (rank == 0) {
       // ------------------------------------------------ MMA issuer
       // Warp-uniform loop; one elected lane issues the MMAs and commits.
-      constexpr uint32_t idesc_full = FP8 ? ptx::umma_idesc_e4m3(C::UMMA_M, C::SN) : ptx::umma_idesc_bf16(C::UMMA_M, C::SN);
-      // Narrow last chunk (S not a multiple of 256): only its columns are computed.
-      const uint32_t idesc_last = NP == 1 ? (FP8 ? ptx::umma_idesc_e4m3(C::UMMA_M, p.n_last)
-                                                 : ptx::umma_idesc_bf16(C::UMMA_M, p.n_last))
-                                          : idesc_full;
+      auto make_idesc = [](int n) {
+        return C::MX ? ptx::umma_idesc_mx(C::UMMA_M, n)
+                     : (FP8 ? ptx::umma_idesc_e4m3(C::UMMA_M, n) : ptx::umma_idesc_bf16(C::UMMA_M, n));
+      };
+      const uint32_t idesc_full = make_idesc(C::SN);
+      // Narrow last chunk (S not a multiple of SN): only its columns are computed.
+      const uint32_t idesc_last = NP == 1 ? make_idesc(p.n_last) : idesc_full;
+      const uint32_t tsfa = tmem_base + C::SF_COL, tsfb = tmem_base + C::SF_COL + 4;
       int st = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -314,7 +345,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         for (int sc = 0; sc < nsc; ++sc) {
           ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), aph ^ 1);
           ptx::tc_fence_after();
-          const uint32_t dt = tmem_base + (uint32_t)(acc * C::SN);
+          const uint32_t dt = tmem_base + (uint32_t)(acc * 256);
           const uint32_t idesc = (sc == nsc - 1) ? idesc_last : idesc_full;
           for (int kb = 0; kb < nkb; ++kb) {
             ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
@@ -323,10 +354,22 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
               const uint32_t sa = ptx::smem_u32(stage_base + st * C::STAGE_BYTES);
               const uint64_t da = ptx::umma_desc_sw128(sa);
               const uint64_t db = ptx::umma_desc_sw128(sa + C::A_BYTES);
+              if constexpr (C::MX) {
+                // Stage scale factors -> TMEM (one slot: tcgen05.cp and
+                // tcgen05.mma of this thread execute in issue order, so the
+                // copy lands after the previous stage's MMAs have read it).
+                const uint32_t ssf = sa + C::A_BYTES + C::B_BYTES;
+                ptx::utccp_32x128b_x4<CG>(tsfa, ptx::smem_desc_rows16(ssf));
+                ptx::utccp_32x128b_x4<CG>(tsfb, ptx::smem_desc_rows16(ssf + 512));
+                ptx::utccp_32x128b_x4<CG>(tsfb + 4, ptx::smem_desc_rows16(ssf + 1024));
+              }
 #pragma unroll
               for (int k = 0; k < C::KSTEPS; ++k) {
                 // +32 bytes along K inside the 128-B swizzle row = +2 in the >>4 address field.
-                if constexpr (FP8) ptx::umma_e4m3<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                if constexpr (C::MX)
+                  ptx::umma_mx<CG>(dt, da + 2 * k, db + 2 * k, ptx::umma_idesc_mx_sf(idesc, k), tsfa, tsfb,
+                                   (kb | k) != 0);
+                else if constexpr (FP8) ptx::umma_e4m3<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
                 else ptx::umma_bf16<CG>(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
               }
               // The stage's H half was written by every pair's producer: release it cluster-wide.
@@ -346,7 +389,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
     // ------------------------------------------------ epilogue (warps 0..3)
     // Dequantisation scale of the raw accumulator (FP8: amax_H/448 * amax_E/448).
     float dscale = 1.0f;
-    if constexpr (FP8) {
+    if constexpr (OP == 1) {
       const float ah = __ldg(p.amax_h), ae = __ldg(p.amax_e);
       dscale = (ah > 0.f ? ah / 448.0f : 1.0f) * (ae > 0.f ? ae / 448.0f : 1.0f);
     }
@@ -376,7 +419,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         // (16 <= S <= 128) occupy the first pack*S columns.
         ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), aph);
         ptx::tc_fence_after();
-        const uint32_t tacc = tq + (uint32_t)(acc * C::SN);
+        const uint32_t tacc = tq + (uint32_t)(acc * 256);
         float cbest = -INFINITY;
         int cidx = 0;
         auto finish_row = [&](int seg) {
@@ -464,18 +507,20 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         // Mask words for the 8 column groups of this chunk (warp-uniform).
         uint32_t keep[8], zero[8];
         if (s0 + C::SN <= p.S) {
-          // Full chunk: one base address, eight byte loads, eight ballots.
+          // Full chunk: one base address, eight byte loads, eight ballots
+          // (MX: group 7 holds 16 positions).
           const uint8_t* mp = mrow + s0 + lane;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            keep[j] = __ballot_sync(0xffffffffu, __ldg(mp + j * 32) != 0);
-            zero[j] = ~keep[j];
+            const bool in = j * 32 + (int)lane < C::SN;
+            keep[j] = __ballot_sync(0xffffffffu, in && __ldg(mp + (in ? j * 32 : 0)) != 0);
+            zero[j] = __ballot_sync(0xffffffffu, in) & ~keep[j];
           }
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int s = s0 + j * 32 + (int)lane;
-            const bool valid = s < p.S;
+            const bool valid = s < p.S && j * 32 + (int)lane < C::SN;
             const bool m = valid && (__ldg(mrow + (valid ? s : 0)) != 0);
             keep[j] = __ballot_sync(0xffffffffu, m);
             zero[j] = __ballot_sync(0xffffffffu, valid && !m);
@@ -485,7 +530,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
         ptx::tc_fence_after();
         float cb[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         int ci[4] = {0, 0, 0, 0};
-        const uint32_t tacc = tq + (uint32_t)(acc * C::SN);
+        const uint32_t tacc = tq + (uint32_t)(acc * 256);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float r[32];
@@ -554,12 +599,12 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
 
 // ------------------------------------------------------------------ host side
 
-template <int CG, int NP, bool FP8>
-int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdParams& prm,
-                    int num_sms, cudaStream_t stream) {
-  using C = FwdCfg<CG, NP, FP8>;
+template <int CG, int NP, int OP>
+int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const CUtensorMap& tmSFA,
+                    const CUtensorMap& tmSFB, const FwdParams& prm, int num_sms, cudaStream_t stream) {
+  using C = FwdCfg<CG, NP, OP>;
   constexpr int CL = CG * NP;   // cluster size
-  auto kern = sparton_fwd_kernel<CG, NP, FP8>;
+  auto kern = sparton_fwd_kernel<CG, NP, OP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(fwd)", e);
   long long want = prm.num_units;
@@ -583,10 +628,10 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
     // Clusters must all be co-resident (static persistent schedule): a GPC
     // with an SM count not divisible by CL leaves SMs no cluster can use, and
     // any cluster beyond the resident limit would run as a serial second wave.
-    static int max_clusters[2][8] = {};
+    static int max_clusters[3][8] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    int& mc = max_clusters[FP8 ? 1 : 0][dev & 7];
+    int& mc = max_clusters[OP][dev & 7];
     if (mc == 0) {
       cfg.gridDim = dim3(grid, 1, 1);
       if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
@@ -599,26 +644,34 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const FwdPar
   if (want < grid / CL) grid = (int)want * CL;
   if (grid < CL) grid = CL;
   cfg.gridDim = dim3(grid, 1, 1);
-  e = cudaLaunchKernelEx(&cfg, kern, tmE, tmH, prm);
+  e = cudaLaunchKernelEx(&cfg, kern, tmE, tmH, tmSFA, tmSFB, prm);
   if (e != cudaSuccess) return set_cuda_error("launch sparton_fwd_kernel", e);
   return SPARTON_OK;
 }
 
 static int gcd_int(int a, int b) { while (b) { const int t = a % b; a = b; b = t; } return a; }
 
-int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cluster_ctas,
-               int num_sms, cudaStream_t stream) {
+int fwd_chunk_cols(int fp8_mode) { return fp8_mode == 2 ? FwdCfg<2, 1, 2>::SN : FwdCfg<2>::SN; }
+
+int fwd_pack(int S, int fp8_mode) {
+  const int sn = fwd_chunk_cols(fp8_mode);
+  return (S >= 16 && S <= 128 && sn / S > 1) ? sn / S : 1;
+}
+
+int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, const CUtensorMap* tmSFA, const CUtensorMap* tmSFB,
+               FwdParams prm, int cluster_ctas, int num_sms, cudaStream_t stream) {
   const int tile_v = 128 * cluster_ctas;
+  const int sn = fwd_chunk_cols(prm.fp8);
   prm.num_vt = (prm.V + tile_v - 1) / tile_v;
-  // Short sequences (16 <= S <= 128): pack floor(256/S) batch rows into one
+  // Short sequences (16 <= S <= 128): pack floor(SN/S) batch rows into one
   // chunk so the MMA computes (almost) no padding columns (SPLADE queries).
-  prm.pack = (prm.S >= 16 && prm.S <= 128) ? 256 / prm.S : 1;
+  prm.pack = fwd_pack(prm.S, prm.fp8);
   if (const char* ev = dev_env("SPARTON_FWD_PACK")) if (ev[0] == '0') prm.pack = 1;
   prm.urows = (prm.B + prm.pack - 1) / prm.pack;
   {
     // UMMA N of the last sequence chunk: the remaining positions rounded up to
     // 16 (cta_group::2 N granularity); packed chunks are always full.
-    const int rem = prm.pack > 1 ? prm.pack * prm.S : prm.S - ((prm.S - 1) / 256) * 256;
+    const int rem = prm.pack > 1 ? prm.pack * prm.S : prm.S - ((prm.S - 1) / sn) * sn;
     prm.n_last = cluster_ctas == 1 ? 256 : ((rem + 15) / 16) * 16;
     if (const char* ev = dev_env("SPARTON_FWD_NLAST")) if (ev[0] == '0') prm.n_last = 256;
   }
@@ -645,14 +698,20 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, in
   if (rot < 1) rot = 1;
   while (gcd_int(rot, nclusters) != 1) ++rot;
   prm.rot = rot % nclusters;
-  if (prm.fp8) {
-    if (cluster_ctas == 4) return launch_fwd_impl<2, 2, true>(tmE, tmH, prm, num_sms, stream);
-    if (cluster_ctas == 2) return launch_fwd_impl<2, 1, true>(tmE, tmH, prm, num_sms, stream);
-    return launch_fwd_impl<1, 1, true>(tmE, tmH, prm, num_sms, stream);
+  const CUtensorMap& sfa = tmSFA ? *tmSFA : tmE;   // unused unless MX
+  const CUtensorMap& sfb = tmSFB ? *tmSFB : tmE;
+  if (prm.fp8 == 2) {
+    if (cluster_ctas != 2 || !tmSFA || !tmSFB) return set_error(SPARTON_EINVAL, "MXFP8 runs on CTA pairs (cta_group 2)");
+    return launch_fwd_impl<2, 1, 2>(tmE, tmH, sfa, sfb, prm, num_sms, stream);
   }
-  if (cluster_ctas == 4) return launch_fwd_impl<2, 2, false>(tmE, tmH, prm, num_sms, stream);
-  if (cluster_ctas == 2) return launch_fwd_impl<2, 1, false>(tmE, tmH, prm, num_sms, stream);
-  return launch_fwd_impl<1, 1, false>(tmE, tmH, prm, num_sms, stream);
+  if (prm.fp8) {
+    if (cluster_ctas == 4) return launch_fwd_impl<2, 2, 1>(tmE, tmH, sfa, sfb, prm, num_sms, stream);
+    if (cluster_ctas == 2) return launch_fwd_impl<2, 1, 1>(tmE, tmH, sfa, sfb, prm, num_sms, stream);
+    return launch_fwd_impl<1, 1, 1>(tmE, tmH, sfa, sfb, prm, num_sms, stream);
+  }
+  if (cluster_ctas == 4) return launch_fwd_impl<2, 2, 0>(tmE, tmH, sfa, sfb, prm, num_sms, stream);
+  if (cluster_ctas == 2) return launch_fwd_impl<2, 1, 0>(tmE, tmH, sfa, sfb, prm, num_sms, stream);
+  return launch_fwd_impl<1, 1, 0>(tmE, tmH, sfa, sfb, prm, num_sms, stream);
 }
 
 // ------------------------------------------------------------------ e4m3 quantisation
@@ -723,8 +782,116 @@ int launch_quantize_e4m3(const void* x, long long n, void* q, float* amax, cudaS
   return SPARTON_OK;
 }
 
+// ------------------------------------------------------------------ MXFP8 quantisation
+// OCP MX block scaling with e4m3 elements: every 32 consecutive K elements of
+// a row share one ue8m0 scale 2^e, the smallest power of two with
+// max|x| / 2^e <= 448 (no saturation), and q = e4m3_rn(x / 2^e).  Scales
+// are written in the layout tcgen05.cp expects for the forward's stages: a
+// 512-B chunk per (128 rows, 4 K blocks) with row r, block k at
+// (r % 32) * 16 + ((r % 128) / 32) * 4 + k.  Rows map to "slots" of
+// slot_rows (128 for E's vocab tiles; 256 for H, one per (unit row, sequence
+// chunk) of the forward's schedule): slot = (r / group_rows) * slots_per_group
+// + (r % group_rows) / chunk_rows, row i = (r % group_rows) % chunk_rows.
+// The scale buffer is zeroed first (unused rows / blocks -> scale 2^-127 x 0).
+struct MxLayout {
+  long long rows;
+  int D, nkg, group_rows, chunk_rows, slots_per_group, slot_rows;
+};
+
+__global__ void __launch_bounds__(256) sparton_quant_mx_kernel(const uint16_t* __restrict__ x, uint8_t* __restrict__ q,
+                                                               uint8_t* __restrict__ sf, const MxLayout L) {
+  const int nblk = (L.D + 31) / 32;
+  const long long total = L.rows * nblk;
+  for (long long t = (long long)blockIdx.x * 256 + threadIdx.x; t < total; t += (long long)gridDim.x * 256) {
+    const long long r = t / nblk;
+    const int blk = (int)(t - r * nblk);
+    const int d0 = blk * 32;
+    const int n = min(32, L.D - d0);               // 32, or 16 for a D % 32 == 16 tail
+    const int4* src = reinterpret_cast<const int4*>(x + r * L.D + d0);
+    uint32_t w[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int4 v = make_int4(0, 0, 0, 0);
+      if (k * 8 < n) v = __ldg(src + k);
+      w[4 * k] = (uint32_t)v.x; w[4 * k + 1] = (uint32_t)v.y; w[4 * k + 2] = (uint32_t)v.z; w[4 * k + 3] = (uint32_t)v.w;
+    }
+    float amax = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(w[k] << 16)), fabsf(__uint_as_float(w[k] & 0xffff0000u))));
+    int e = -127;
+    if (amax > 0.f) {
+      int ex;
+      frexpf(amax, &ex);                            // amax in [2^(ex-1), 2^ex)
+      e = ex - 9 + (ldexpf(amax, 9 - ex) > 448.0f ? 1 : 0);
+      e = max(-127, min(127, e));
+    }
+    const float inv = ldexpf(1.0f, -e);
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint16_t p0 = e4m3x2(__uint_as_float(w[2 * k] << 16) * inv, __uint_as_float(w[2 * k] & 0xffff0000u) * inv);
+      const uint16_t p1 = e4m3x2(__uint_as_float(w[2 * k + 1] << 16) * inv,
+                                 __uint_as_float(w[2 * k + 1] & 0xffff0000u) * inv);
+      o[k] = (uint32_t)p0 | ((uint32_t)p1 << 16);
+    }
+    int4* dst = reinterpret_cast<int4*>(q + r * L.D + d0);
+    dst[0] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
+    if (n > 16) dst[1] = make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]);
+    const long long g = r / L.group_rows;
+    const int within = (int)(r - g * L.group_rows);
+    const long long slot = g * L.slots_per_group + within / L.chunk_rows;
+    const int i = within % L.chunk_rows;
+    const long long off = ((slot * L.nkg + blk / 4) * (L.slot_rows / 128) + i / 128) * 512 + (i % 32) * 16 +
+                          ((i % 128) / 32) * 4 + (blk % 4);
+    sf[off] = (uint8_t)(e + 127);
+  }
+}
+
+static MxLayout mx_layout(bool h_operand, long long rows_or_B, long long S, int D) {
+  MxLayout L{};
+  L.D = D;
+  L.nkg = (D + 127) / 128;
+  if (h_operand) {
+    const int sn = fwd_chunk_cols(2), pack = fwd_pack((int)S, 2);
+    L.rows = rows_or_B * S;
+    L.group_rows = (int)(pack * S);
+    L.chunk_rows = sn;
+    L.slots_per_group = pack > 1 ? 1 : (int)((S + sn - 1) / sn);
+    L.slot_rows = 256;
+  } else {
+    L.rows = rows_or_B;
+    L.group_rows = 128;
+    L.chunk_rows = 128;
+    L.slots_per_group = 1;
+    L.slot_rows = 128;
+  }
+  return L;
+}
+
+long long mx_sf_bytes(bool h_operand, long long rows_or_B, long long S, int D) {
+  const MxLayout L = mx_layout(h_operand, rows_or_B, S, D);
+  const long long groups = (L.rows + L.group_rows - 1) / L.group_rows;
+  return groups * L.slots_per_group * L.nkg * (L.slot_rows / 128) * 512;
+}
+
+int launch_quantize_mx(bool h_operand, const void* x, long long rows_or_B, long long S, int D, void* q, void* sf,
+                       cudaStream_t stream) {
+  const MxLayout L = mx_layout(h_operand, rows_or_B, S, D);
+  cudaError_t e = cudaMemsetAsync(sf, 0, (size_t)mx_sf_bytes(h_operand, rows_or_B, S, D), stream);
+  if (e != cudaSuccess) return set_cuda_error("cudaMemsetAsync(mx scales)", e);
+  const long long work = L.rows * ((D + 31) / 32);
+  int blocks = (int)std::min<long long>((work + 255) / 256, 148ll * 16);
+  if (blocks < 1) blocks = 1;
+  sparton_quant_mx_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(x), static_cast<uint8_t*>(q),
+                                                       static_cast<uint8_t*>(sf), L);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("launch mx quantisation", e);
+  return SPARTON_OK;
+}
+
 // Rows of H each CTA loads per TMA box for a cluster of `cluster_ctas` CTAs.
-int fwd_h_box_rows(int cluster_ctas) { return 256 / cluster_ctas; }
+int fwd_h_box_rows(int cluster_ctas, int fp8_mode) { return fwd_chunk_cols(fp8_mode) / cluster_ctas; }
 
 int fwd_smem_bytes(int cluster_ctas) {
   return cluster_ctas >= 2 ? FwdCfg<2>::SMEM_BYTES : FwdCfg<1>::SMEM_BYTES;

@@ -39,7 +39,8 @@ struct FwdParams {
   int pack;            // batch rows per 256-position chunk (S = 256/pack in {32, 64, 128}), else 1
   int urows;           // unit rows: B (pack == 1) or ceil(B / pack) batch-row groups
   int n_last;          // UMMA N of a unit's last sequence chunk (multiple of 16, <= 256)
-  int fp8;             // 1: H and E are e4m3 (kind::f8f6f4), dequantised by amax_h/448 * amax_e/448
+  int fp8;             // 1: H and E are e4m3 (kind::f8f6f4), dequantised by amax_h/448 * amax_e/448;
+                       // 2: MXFP8 (kind::mxf8f6f4.block_scale, ue8m0 scales per 32 K elements)
   const float* amax_h; // device scalars (FP8 only)
   const float* amax_e;
 };
@@ -103,11 +104,20 @@ const char* dev_env(const char* name);
 int set_error(int code, const char* msg);
 int set_cuda_error(const char* what, cudaError_t e);
 
-int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, FwdParams prm, int cluster_ctas,
-               int num_sms, cudaStream_t stream);
+// tmSFA / tmSFB: the MXFP8 scale-factor maps (prm.fp8 == 2), else nullptr.
+int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, const CUtensorMap* tmSFA, const CUtensorMap* tmSFB,
+               FwdParams prm, int cluster_ctas, int num_sms, cudaStream_t stream);
 int launch_quantize_e4m3(const void* x, long long n, void* q, float* amax, cudaStream_t stream);
 int fwd_smem_bytes(int cluster_ctas);
-int fwd_h_box_rows(int cluster_ctas);
+int fwd_h_box_rows(int cluster_ctas, int fp8_mode);
+// Sequence positions per forward chunk (256; MXFP8: 240) and the short-sequence packing factor.
+int fwd_chunk_cols(int fp8_mode);
+int fwd_pack(int S, int fp8_mode);
+// MXFP8 operands: scale-factor bytes and the quantiser (h_operand: H as
+// (B, S, D) laid out per the forward's (unit row, chunk) slots; else E (V, D)).
+long long mx_sf_bytes(bool h_operand, long long rows_or_B, long long S, int D);
+int launch_quantize_mx(bool h_operand, const void* x, long long rows_or_B, long long S, int D, void* q, void* sf,
+                       cudaStream_t stream);
 // H viewed as (B*S) x D bf16 with a (64 x rows) box, no swizzle (staged dE tiles).
 int encode_bf16_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long long cols, int box_rows,
                          int box_cols);

@@ -21,6 +21,9 @@ from . import _lib
 __all__ = [
     "sparton_forward",
     "sparton_forward_fp8",
+    "sparton_forward_mx",
+    "quantize_mx",
+    "dequantize_mx",
     "quantize_e4m3",
     "sparton_backward",
     "sparton_forward_fp32",
@@ -181,6 +184,102 @@ def _fwd_fp8_launch(qH, aH, qE, aE, bias, m, Y, I, cta_group=0):
                                  _stream_ptr())
     _lib.check(rc)
     return Y, I
+
+
+@torch.no_grad()
+def quantize_mx(x: torch.Tensor, operand: str) -> tuple[torch.Tensor, torch.Tensor]:
+    """MXFP8 quantisation on the GPU (OCP MX, e4m3 elements, one ue8m0 scale
+    per 32 consecutive elements of a row): returns (q uint8 view of e4m3
+    values shaped like x, sf uint8 scale bytes in the forward's tcgen05.cp
+    layout).  ``operand`` "H" for a (B, S, D) hidden-state tensor, "E" for the
+    (V, D) vocabulary matrix.  x ~= q * 2^(sf - 127) blockwise."""
+    _require_cuda("x", x)
+    if x.dtype != torch.bfloat16:
+        raise ValueError(f"x must be bfloat16, got {x.dtype}")
+    if operand == "H":
+        if x.dim() != 3:
+            raise ValueError("H must be (B, S, D)")
+        (B, S, D), V, op = x.shape, 1, _lib.SPARTON_MX_H
+    elif operand == "E":
+        if x.dim() != 2:
+            raise ValueError("E must be (V, D)")
+        (V, D), B, S, op = x.shape, 1, 1, _lib.SPARTON_MX_E
+    else:
+        raise ValueError(f"operand must be 'H' or 'E', got {operand!r}")
+    lib = _lib.load()
+    nsf = int(lib.sparton_mx_scales_bytes(B, S, D, V, op))
+    if nsf <= 0:
+        raise ValueError(f"bad shape {tuple(x.shape)}")
+    xc = x.contiguous()
+    q = torch.empty(xc.shape, dtype=torch.uint8, device=x.device)
+    sf = torch.empty(nsf, dtype=torch.uint8, device=x.device)
+    with torch.cuda.device(x.device):
+        rc = lib.sparton_quantize_mx(xc.data_ptr(), B, S, D, V, op, q.data_ptr(), sf.data_ptr(), nsf,
+                                     _stream_ptr())
+    _lib.check(rc)
+    return q, sf
+
+
+def mx_scale_index(shape, operand: str, S: int | None = None):
+    """Host-side restatement of the scale layout (sparton_quant_mx_kernel):
+    for every (row, 32-element block) of x, the byte offset of its scale in
+    ``sf``.  Returns an int64 tensor of shape (rows, ceil(D / 32)).  Used by
+    ``dequantize_mx`` and the tests."""
+    if operand == "H":
+        B, S_, D = shape
+        rows = B * S_
+        sn = 240
+        pack = sn // S_ if (16 <= S_ <= 128 and sn // S_ > 1) else 1
+        group, chunk, spg, slot_rows = pack * S_, sn, (1 if pack > 1 else -(-S_ // sn)), 256
+    else:
+        V, D = shape
+        rows, group, chunk, spg, slot_rows = V, 128, 128, 1, 128
+    nkg = -(-D // 128)
+    r = torch.arange(rows, dtype=torch.int64).unsqueeze(1)
+    blk = torch.arange(-(-D // 32), dtype=torch.int64).unsqueeze(0)
+    g, within = r // group, r % group
+    slot, i = g * spg + within // chunk, within % chunk
+    return (((slot * nkg + blk // 4) * (slot_rows // 128) + i // 128) * 512 + (i % 32) * 16 +
+            ((i % 128) // 32) * 4 + blk % 4)
+
+
+def dequantize_mx(q: torch.Tensor, sf: torch.Tensor, operand: str) -> torch.Tensor:
+    """float32 values of an MX-quantised operand: q (e4m3 bytes) x 2^(sf-127)."""
+    shape = tuple(q.shape)
+    D = shape[-1]
+    vals = q.view(torch.float8_e4m3fn).float().reshape(-1, D)
+    idx = mx_scale_index(shape, operand).to(q.device)
+    e = sf.to(torch.int64)[idx].float() - 127.0                 # (rows, nblk)
+    scale = torch.exp2(e).repeat_interleave(32, dim=1)[:, :D]
+    return (vals * scale).reshape(shape)
+
+
+@torch.no_grad()
+def sparton_forward_mx(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor, *,
+                       E_q: tuple[torch.Tensor, torch.Tensor] | None = None, return_quantized: bool = False):
+    """MXFP8 variant of the fused forward: H and E
+    quantised with per-32-element ue8m0 block scales (``quantize_mx``), the
+    tensor cores apply the scales (tcgen05.mma kind::mxf8f6f4.block_scale).
+    Y/I follow the definition of ``sparton_forward`` on the dequantised
+    operands.  ``E_q`` may pass a cached ``quantize_mx(E, "E")``;
+    ``return_quantized`` also returns (qH, sfH, qE, sfE)."""
+    B, S, D, V = _check_inputs(H, E, bias, mask)
+    if D % 16:
+        raise ValueError("the MXFP8 forward needs D to be a multiple of 16")
+    qH, sH = quantize_mx(H, "H")
+    qE, sE = E_q if E_q is not None else quantize_mx(E, "E")
+    m = mask.contiguous()
+    if m.dtype == torch.bool:
+        m = m.view(torch.uint8)
+    bias = bias.contiguous()
+    Y = torch.empty((B, V), dtype=torch.float32, device=H.device)
+    I = torch.empty((B, V), dtype=torch.int32, device=H.device)
+    lib = _lib.load()
+    with torch.cuda.device(H.device):
+        rc = lib.sparton_fwd_mx(qH.data_ptr(), sH.data_ptr(), qE.data_ptr(), sE.data_ptr(), bias.data_ptr(),
+                                m.data_ptr(), Y.data_ptr(), I.data_ptr(), B, S, D, V, V, _stream_ptr())
+    _lib.check(rc)
+    return ((Y, I), (qH, sH, qE, sE)) if return_quantized else (Y, I)
 
 
 @torch.no_grad()

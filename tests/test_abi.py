@@ -24,7 +24,8 @@ def test_header_declares_entry_points():
     assert names == sorted(["sparton_abi_version", "sparton_last_error", "sparton_device_sm_count",
                             "sparton_fwd", "sparton_fwd_fp8", "sparton_fwd_multi", "sparton_quantize_e4m3",
                             "sparton_bwd_workspace_bytes", "sparton_bwd", "sparton_bwd_ex",
-                            "sparton_bwd_fp8"])
+                            "sparton_bwd_fp8", "sparton_mx_scales_bytes", "sparton_quantize_mx",
+                            "sparton_fwd_mx"])
 
 
 def test_library_exports_every_declared_symbol():
@@ -115,6 +116,22 @@ def test_fp8_entry_points_reject_bad_arguments_before_any_cuda_call():
     assert lib.sparton_fwd_fp8(d, d, None, d, d, d, d, d, 2, 3, 16, 5, 5, 0, None) == _lib.SPARTON_EINVAL
     assert lib.sparton_quantize_e4m3(d, 15, d, d, None) == _lib.SPARTON_EINVAL
     assert lib.sparton_quantize_e4m3(d, 0, d, d, None) == _lib.SPARTON_EINVAL
+
+
+def test_mx_entry_points_reject_bad_arguments_before_any_cuda_call():
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    d = ctypes.c_void_p(16)
+    # scale bytes: E (V, D) = ceil(V/128) * ceil(D/128) chunks of 512 B; H per (batch row, 240-position chunk)
+    assert lib.sparton_mx_scales_bytes(1, 1, 768, 250002, _lib.SPARTON_MX_E) == 1954 * 6 * 512
+    assert lib.sparton_mx_scales_bytes(512, 512, 768, 1, _lib.SPARTON_MX_H) == 512 * 3 * 6 * 1024
+    assert lib.sparton_mx_scales_bytes(8, 32, 64, 1, _lib.SPARTON_MX_H) == 2 * 1 * 1 * 1024   # 7 rows per chunk
+    assert lib.sparton_mx_scales_bytes(8, 32, 64, 1, 7) == 0
+    assert lib.sparton_quantize_mx(d, 2, 3, 8, 5, _lib.SPARTON_MX_H, d, d, 1 << 20, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_quantize_mx(d, 2, 3, 16, 5, 9, d, d, 1 << 20, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_quantize_mx(d, 2, 3, 16, 5, _lib.SPARTON_MX_E, d, d, 1, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_fwd_mx(d, d, d, d, d, d, d, d, 2, 3, 8, 5, 5, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_fwd_mx(d, None, d, d, d, d, d, d, 2, 3, 16, 5, 5, None) == _lib.SPARTON_EINVAL
 
 
 def test_experiment_switches_need_the_dev_gate(monkeypatch):
