@@ -47,6 +47,7 @@ from pathlib import Path
 
 REPO = Path(__file__).resolve().parent
 CONFIGS = {
+    "cfg1": dict(B=8, S=128, D=768, V=30522),
     "cfg2": dict(B=512, S=512, D=768, V=30522),
     "cfg3": dict(B=512, S=512, D=768, V=250002),
     "cfg4": dict(B=2048, S=512, D=1024, V=250002),
@@ -60,9 +61,12 @@ def flops(c):
 
 
 def config_dict(cname, c, world):
+    h, e, dy = c["B"] * c["S"] * c["D"] * 2, c["V"] * c["D"] * 2, c["B"] * c["V"] * 4
+    sizes = "H %d MiB, E %d MiB, dY %d MiB" % (h >> 20, e >> 20, dy >> 20)
+    l2 = ("inputs larger than L2 (%s)" % sizes if h + e + dy > (126 << 20)
+          else "no flush: inputs fit in L2 (%s), warm-cache steps" % sizes)
     return {"workload": cname, **c, "parallelism": f"vocab-shard{world}" if world > 1 else "single",
-            "l2_flush": "inputs larger than L2 (H %d MiB, E %d MiB, dY %d MiB)" % (
-                c["B"] * c["S"] * c["D"] * 2 >> 20, c["V"] * c["D"] * 2 >> 20, c["B"] * c["V"] * 4 >> 20)}
+            "l2_flush": l2}
 
 
 SPARSE_BIAS = -2.0   # SURVEY §8d "SPLADE-sparse" variant
@@ -265,8 +269,33 @@ def run_reference_arm(args, c, cname):
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "sample_seconds_median": t,
     }
+    if cname != "cfg1" and not args.no_cfg1 and arm.kind == "reference":
+        line["cfg1"] = reference_cfg1(arm.threads)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def reference_cfg1(threads, steps=2):
+    """BASELINE configs[0], the reference's own CPU case, timed in FULL (no
+    extrapolation): the stock forward_hybrid + backward_fused on the
+    reference's exact cfg1 inputs (HeadInputs.seeded(Dims(8,128,768,30522),
+    0, mask_keep=0.85), dY = seeded_tensor((B, V), 9))."""
+    fh = _reference_module()
+    dims = fh.Dims(8, 128, 768, 30522)
+    inputs = fh.HeadInputs.seeded(dims, 0, mask_keep=0.85)
+    dY = fh.seeded_tensor((dims.B, dims.V), 9)
+    cfg = fh.TileConfig.default_for(dims, num_threads=threads)
+    ts = []
+    for _ in range(steps + 1):
+        t0 = time.perf_counter()
+        out = fh.forward_hybrid(inputs, cfg)
+        fh.backward_fused(inputs, fh.SavedSparseState.from_output(out), dY, cfg)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts[1:])
+    ff, fb = flops(CONFIGS["cfg1"])
+    return {"config": config_dict("cfg1", CONFIGS["cfg1"], 1), "ms_per_step": t * 1e3,
+            "value": (ff + fb) / t / 1e12, "unit": "TFLOP/s", "steps": steps, "cores": threads,
+            "note": "stock reference forward_hybrid + backward_fused at cfg1 in full (f32), no extrapolation"}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -470,6 +499,8 @@ def run_gpu_arm(args, c, cname):
                         "value": (f4 + b4) / (ms4 * 1e-3) / 1e12, "unit": "TFLOP/s", "steps": args.steps,
                         "peak_hbm_bytes": peak4,
                         "gpu_launches": launches_per_step(c4, -(-c4["V"] // world)) * args.steps * world}
+    if world == 1 and cname != "cfg1" and not args.no_cfg1:
+        line["cfg1"] = gpu_cfg1(dev, args.steps, args.warmup)
     if rank == 0 and world == 1 and not args.no_cpu:
         arm = CpuArm(c)
         line["cpu_baseline"] = arm.describe(arm.sample())
@@ -479,6 +510,41 @@ def run_gpu_arm(args, c, cname):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def gpu_cfg1(dev, steps, warmup):
+    """BASELINE configs[0] (B=8, S=128, D=768, V=30522) on the GPU beside the
+    reference arm's full cfg1 record: the bf16 path and the fp32-accuracy path
+    (the reference's dtype contract), fwd + bwd per step, CUDA events."""
+    import torch
+    from paper_2603_25011_b200 import (sparton_backward, sparton_backward_fp32, sparton_forward,
+                                       sparton_forward_fp32)
+    c = CONFIGS["cfg1"]
+    B, S, D, V = c["B"], c["S"], c["D"], c["V"]
+    g = torch.Generator(device=dev).manual_seed(0)
+    H = torch.rand((B, S, D), generator=g, device=dev) * 2 - 1
+    E = torch.rand((V, D), generator=g, device=dev) * 2 - 1
+    b = torch.rand(V, generator=g, device=dev) * 2 - 1
+    m = (torch.rand((B, S), generator=g, device=dev) < 0.85).to(torch.uint8)
+    dY = torch.rand((B, V), generator=g, device=dev) * 2 - 1
+    Hb, Eb = H.to(torch.bfloat16), E.to(torch.bfloat16)
+    runs = {"bf16": lambda: sparton_backward(Hb, Eb, *sparton_forward(Hb, Eb, b, m), dY),
+            "fp32_accuracy": lambda: sparton_backward_fp32(H, E, *sparton_forward_fp32(H, E, b, m), dY)}
+    ff, fb = flops(c)
+    rec = {"config": config_dict("cfg1", c, 1), "steps": steps, "unit": "TFLOP/s"}
+    for name, fn in runs.items():
+        for _ in range(max(3, warmup)):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        rec[name] = {"ms_per_step": ms, "value": (ff + fb) / (ms * 1e-3) / 1e12}
+    return rec
 
 
 def run_e2e(args, c, dev, rank, world):
@@ -620,6 +686,7 @@ def main() -> int:
     ap.add_argument("--no-cfg4", action="store_true", help="N>1: skip the cfg4 record")
     ap.add_argument("--no-fused-ab", action="store_true", help="N>1: skip the fused all-gather A/B record")
     ap.add_argument("--no-sparse", action="store_true", help="N=1: skip the SPLADE-sparse (bias -2) record")
+    ap.add_argument("--no-cfg1", action="store_true", help="N=1: skip the cfg1 (reference CPU case) record")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":

@@ -11,7 +11,7 @@ Public surface:
   * vocab-sharded multi-GPU head: ``paper_2603_25011_b200.sharded``
 """
 
-from .head import (SpartonHeadFn, SpartonHeadFp8Fn, bwd_workspace_bytes, dequantize_mx, quantize_e4m3, quantize_mx,
+from .head import (SpartonHeadFn, SpartonHeadFp8Fn, SpartonHeadMxFn, sparton_head_mx, bwd_workspace_bytes, dequantize_mx, quantize_e4m3, quantize_mx,
                    sparton_backward, sparton_backward_fp8, sparton_backward_fp32, sparton_forward,
                    sparton_forward_fp8, sparton_forward_fp32, sparton_forward_mx, sparton_head, sparton_head_fp8,
                    split_bf16x3)
@@ -32,6 +32,8 @@ __all__ = [
     "sparton_forward_fp8",
     "quantize_e4m3",
     "sparton_forward_mx",
+    "SpartonHeadMxFn",
+    "sparton_head_mx",
     "quantize_mx",
     "dequantize_mx",
     "sparton_head",

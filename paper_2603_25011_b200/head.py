@@ -31,6 +31,8 @@ __all__ = [
     "sparton_backward_fp8",
     "SpartonHeadFp8Fn",
     "sparton_head_fp8",
+    "SpartonHeadMxFn",
+    "sparton_head_mx",
     "split_bf16x3",
     "SpartonHeadFn",
     "sparton_head",
@@ -517,6 +519,30 @@ class SpartonHeadFp8Fn(torch.autograd.Function):
         dH, dE, db = sparton_backward_fp8(qH, aH, qE, aE, Y, I, dY.float(),
                                           include_bias_grad=ctx.include_bias_grad, grad_dtype=ctx.dtypes[0])
         return dH, dE.to(ctx.dtypes[1]), db, None, None
+
+
+class SpartonHeadMxFn(torch.autograd.Function):
+    """MXFP8 autograd op: the block-scaled e4m3 forward (``sparton_forward_mx``)
+    and the bf16 argmax-routed backward on the caller's bf16 H, E at the MX
+    forward's (Y, I) — the usual low-precision recipe (FP8 forward, bf16
+    backward), straight-through w.r.t. the quantisation.  Saved state is the
+    same B·V·8 bytes as ``SpartonHeadFn``."""
+
+    @staticmethod
+    def forward(ctx, H, E, bias, mask, include_bias_grad=True):
+        Y, I = sparton_forward_mx(H, E, bias, mask)
+        ctx.save_for_backward(H, E, Y, I)
+        ctx.include_bias_grad = bool(include_bias_grad)
+        ctx.mark_non_differentiable(I)
+        return Y, I
+
+    backward = staticmethod(SpartonHeadFn.backward)
+
+
+def sparton_head_mx(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,
+                    include_bias_grad: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
+    """Functional MXFP8 head: (Y, I) with autograd through Y (``SpartonHeadMxFn``)."""
+    return SpartonHeadMxFn.apply(H, E, bias, mask, include_bias_grad)
 
 
 def sparton_head_fp8(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,

@@ -129,3 +129,21 @@ def test_mx_vs_bf16_and_per_tensor_fp8(cuda_device):
                      float((I8 == I16).float().mean()))
     print("vs bf16 (median rel |dY|, argmax agreement):", out)
     assert out["mx"][0] < 0.05 and out["mx"][1] > 0.5
+
+
+def test_mx_autograd_head(cuda_device):
+    """SpartonHeadMxFn: MX forward, bf16 backward at the MX forward's (Y, I)."""
+    from paper_2603_25011_b200 import sparton_backward, sparton_forward_mx, sparton_head_mx
+    g = torch.Generator(device="cuda").manual_seed(9)
+    B, S, D, V = 3, 300, 256, 4000
+    H = torch.randn((B, S, D), generator=g, device="cuda").to(torch.bfloat16).requires_grad_()
+    E = (torch.randn((V, D), generator=g, device="cuda") * 0.05).to(torch.bfloat16).requires_grad_()
+    b = torch.zeros(V, device="cuda", requires_grad=True)
+    m = torch.ones((B, S), dtype=torch.uint8, device="cuda")
+    Y, I = sparton_head_mx(H, E, b, m)
+    Y0, I0 = sparton_forward_mx(H.detach(), E.detach(), b.detach(), m)
+    assert torch.equal(Y, Y0) and torch.equal(I, I0)
+    dY = torch.randn((B, V), generator=g, device="cuda")
+    Y.backward(dY)
+    dH, dE, db = sparton_backward(H.detach(), E.detach(), Y0, I0, dY, grad_dtype=torch.bfloat16)
+    assert torch.equal(H.grad, dH) and torch.equal(E.grad, dE.to(E.dtype)) and torch.equal(b.grad, db)
