@@ -339,7 +339,9 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False, bi
     """Warm up, then time `steps` fwd+bwd steps between barriers; returns
     (ms per step, mean forward ms, peak bytes, head-owned peak bytes, inputs).
     ``fused``: N > 1 with the (Y, I) all-gather fused into K1's epilogue
-    (sharded.FusedVocabGather) instead of NCCL all-gather + permute copy."""
+    (sharded.FusedVocabGather) instead of NCCL all-gather + permute copy:
+    "p2p" stores to every peer's buffer, "nvls" one multimem store per result
+    through the multicast mapping."""
     import torch
     import torch.distributed as dist
     from paper_2603_25011_b200 import sharded, sparton_backward, sparton_forward
@@ -348,7 +350,7 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False, bi
     H, E, bias, mask, dY, (v0, v1, Vp) = make_inputs(c, dev, rank, world, bias_value)
     stream = torch.cuda.current_stream()
     fwd_ev = [] if fwd_ev is None else fwd_ev
-    fg = sharded.FusedVocabGather.symmetric(c["B"], V, dev) if fused else None
+    fg = sharded.FusedVocabGather.symmetric(c["B"], V, dev, multicast=(fused == "nvls")) if fused else None
 
     def step(timed=False):
         if timed:
@@ -464,13 +466,23 @@ def run_gpu_arm(args, c, cname):
         # A/B of the NVLink-fused (Y, I) all-gather on the
         # same workload; the headline keeps the NCCL path.
         try:
-            msf, fwdf, _, _, inpf = timed_steps(c, dev, rank, world, args.steps, args.warmup, fused=True)
+            msf, fwdf, _, _, inpf = timed_steps(c, dev, rank, world, args.steps, args.warmup, fused="p2p")
             del inpf
             line["fused_gather"] = {"ms_per_step": msf, "fwd_ms": fwdf, "value": (ff + fb) / (msf * 1e-3) / 1e12,
                                     "unit": "TFLOP/s", "note": "K1 epilogue stores into every rank's symmetric "
                                     "[B, V] buffers (sparton_fwd_multi) instead of NCCL all-gather"}
         except Exception as exc:
             line["fused_gather"] = {"unavailable": repr(exc)[:300]}
+        torch.cuda.empty_cache()
+        try:
+            msn, fwdn, _, _, inpn = timed_steps(c, dev, rank, world, args.steps, args.warmup, fused="nvls")
+            del inpn
+            line["nvls_gather"] = {"ms_per_step": msn, "fwd_ms": fwdn, "value": (ff + fb) / (msn * 1e-3) / 1e12,
+                                   "unit": "TFLOP/s", "note": "K1 epilogue stores each result once with "
+                                   "multimem.st to the symmetric buffers' NVLS multicast mapping "
+                                   "(sparton_fwd_multicast)"}
+        except Exception as exc:
+            line["nvls_gather"] = {"unavailable": repr(exc)[:300]}
         torch.cuda.empty_cache()
     if world == 1 and not args.no_sparse:
         # SURVEY §8d secondary run: the SPLADE-sparse variant (bias -2: a few %

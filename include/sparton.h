@@ -101,8 +101,8 @@ SPARTON_API int sparton_fwd_fp8(const void* H8, const void* E8, const float* ama
  * one row stride ldY: Y_dst[k] / I_dst[k] are device pointers (host array of
  * pointers) to the first column this call covers.  For a vocab-sharded head
  * they are the peers' symmetric [B, V] buffers offset to this shard's first
- * column (P2P-mapped over NVLink), or one NVLS multicast address — the
- * (Y, I) all-gather is fused into the epilogue's stores.  Destinations must
+ * column (P2P-mapped over NVLink) — the (Y, I) all-gather is fused into the
+ * epilogue's stores (multicast addresses: sparton_fwd_multicast).  Destinations must
  * not overlap.  Replaces no reference function (the reference has no
  * multi-device path); see INTEGRATION.md.
  */
@@ -110,6 +110,19 @@ SPARTON_API int sparton_fwd_multi(const void* H, const void* E, const float* bia
                                   int ndst, float* const* Y_dst, int32_t* const* I_dst,
                                   int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY,
                                   int cta_group, void* stream);
+
+/*
+ * sparton_fwd storing every (b, v) result with multimem.st.relaxed.sys to
+ * NVLink SHARP multicast addresses Y_mc / I_mc (first column this call covers,
+ * row stride ldY): the multicast object binds every rank's symmetric [B, V]
+ * buffer, so one store per result lands in all ranks' copies — the (Y, I)
+ * all-gather of a vocab-sharded head done by the switch inside the epilogue.
+ * Needs an NVLS-capable NVSwitch system (a multicast object of >= 2 GPUs);
+ * otherwise identical to sparton_fwd.  No reference counterpart.
+ */
+SPARTON_API int sparton_fwd_multicast(const void* H, const void* E, const float* bias, const uint8_t* mask,
+                                      float* Y_mc, int32_t* I_mc, int64_t B, int64_t S, int64_t D, int64_t V,
+                                      int64_t ldY, int cta_group, void* stream);
 
 /* Per-tensor e4m3 quantisation of n bf16 values (n a multiple of 16, 16-B
  * aligned): amax (device f32 scalar) = max |x|, q = e4m3(x * 448 / amax). */

@@ -42,6 +42,7 @@ EXPORTED = (
     "sparton_fwd",
     "sparton_fwd_fp8",
     "sparton_fwd_multi",
+    "sparton_fwd_multicast",
     "sparton_quantize_e4m3",
     "sparton_bwd_workspace_bytes",
     "sparton_bwd",
@@ -86,6 +87,8 @@ def load() -> ctypes.CDLL:
         lib.sparton_fwd_multi.restype = c_int
         lib.sparton_fwd_multi.argtypes = [c_vp, c_vp, c_vp, c_vp, c_int, ctypes.POINTER(c_vp),
                                           ctypes.POINTER(c_vp), c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]
+        lib.sparton_fwd_multicast.restype = c_int
+        lib.sparton_fwd_multicast.argtypes = [c_vp] * 6 + [c_i64] * 5 + [c_int, c_vp]
         lib.sparton_fwd_fp8.restype = c_int
         lib.sparton_fwd_fp8.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                         c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]

@@ -198,7 +198,7 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
                       const uint8_t* mask, float* Y, int32_t* I, int64_t B, int64_t S, int64_t D, int64_t V,
                       int64_t ldY, int cta_group, void* stream, int fp8, int nx = 0,
                       float* const* Yx = nullptr, int32_t* const* Ix = nullptr, const void* Hsf = nullptr,
-                      const void* Esf = nullptr) {
+                      const void* Esf = nullptr, bool multicast = false) {
   int rc = check_dims(B, S, D, V);
   if (rc) return rc;
   if (!H || !E || !bias || !mask || !Y || !I) return set_error(SPARTON_EINVAL, "null pointer argument");
@@ -253,6 +253,7 @@ static int fwd_common(const void* H, const void* E, const float* amax_h, const f
   prm.ldY = ldY;
   prm.fp8 = fp8;
   prm.nx = nx;
+  prm.mc = multicast ? 1 : 0;
   for (int k = 0; k < nx; ++k) {
     prm.Yx[k] = Yx[k];
     prm.Ix[k] = Ix[k];
@@ -282,6 +283,13 @@ int sparton_fwd_multi(const void* H, const void* E, const float* bias, const uin
     return set_error(SPARTON_EINVAL, "ndst must lie in [1, 8] with non-null destination arrays");
   return fwd_common(H, E, nullptr, nullptr, bias, mask, Y_dst[0], I_dst[0], B, S, D, V, ldY, cta_group, stream,
                     0, ndst - 1, Y_dst + 1, I_dst + 1);
+}
+
+int sparton_fwd_multicast(const void* H, const void* E, const float* bias, const uint8_t* mask, float* Y_mc,
+                          int32_t* I_mc, int64_t B, int64_t S, int64_t D, int64_t V, int64_t ldY, int cta_group,
+                          void* stream) {
+  return fwd_common(H, E, nullptr, nullptr, bias, mask, Y_mc, I_mc, B, S, D, V, ldY, cta_group, stream, 0, 0,
+                    nullptr, nullptr, nullptr, nullptr, true);
 }
 
 int sparton_fwd_fp8(const void* H8, const void* E8, const float* amax_h, const float* amax_e, const float* bias,

@@ -191,9 +191,15 @@ __device__ __forceinline__ void reduce_group_fast(const float (&r)[32], int c0, 
 
 // One (b, v) result: the caller's output plus any extra destinations (the
 // peers' [B, V] copies of a vocab-sharded head, written over NVLink — the
-// all-gather fused into the epilogue).  Consecutive lanes hold consecutive v,
+// all-gather fused into the epilogue), or one multimem store to a multicast
+// address that the NVSwitch replicates to every rank's copy.  Consecutive lanes hold consecutive v,
 // so every destination sees the same coalesced 128-B row segments.
 __device__ __forceinline__ void store_yi(const FwdParams& p, size_t o, float y, int i) {
+  if (p.mc) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" :: "l"(p.Y + o), "f"(y) : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.s32 [%0], %1;" :: "l"(p.I + o), "r"(i) : "memory");
+    return;
+  }
   p.Y[o] = y;
   p.I[o] = i;
   for (int k = 0; k < p.nx; ++k) {

@@ -27,6 +27,10 @@ struct FwdParams {
   int nx;
   float* Yx[kMaxFwdDst - 1];
   int32_t* Ix[kMaxFwdDst - 1];
+  // mc = 1: Y / I are NVLink SHARP multicast addresses (a symmetric [B, V]
+  // buffer bound on every rank): one multimem.st per result reaches every
+  // rank's copy, the all-gather done by the switch (nx must be 0).
+  int mc;
   int B, S, D, V;
   long long ldY;
   int num_vt;          // number of vocab tiles

@@ -84,7 +84,7 @@ def _check_inputs(H, E, bias, mask):
 @torch.no_grad()
 def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: torch.Tensor,
                     *, cta_group: int = 0, out: tuple[torch.Tensor, torch.Tensor] | None = None,
-                    extra_out: tuple[tuple[int, int], ...] = ()
+                    extra_out: tuple[tuple[int, int], ...] = (), multicast_out: tuple[int, int] | None = None
                     ) -> tuple[torch.Tensor, torch.Tensor]:
     """Fused head forward: returns (Y f32 [B, V], I int32 [B, V]).
 
@@ -94,6 +94,10 @@ def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: 
     stride).  ``extra_out`` lists up to 7 more (Y, I) device addresses (raw
     pointers, same row stride as ``out``) that receive identical stores —
     the peers' copies of a vocab-sharded head's output (``sparton_fwd_multi``).
+    ``multicast_out`` = (Y, I) NVLS multicast addresses of the same columns
+    (row stride of ``out``): results are stored there with multimem.st only —
+    the switch writes every rank's copy, ``out`` included
+    (``sparton_fwd_multicast``).
     """
     B, S, D, V = _check_inputs(H, E, bias, mask)
     Hp = _pad_hidden(H.contiguous()).reshape(B * S, -1)
@@ -114,8 +118,14 @@ def sparton_forward(H: torch.Tensor, E: torch.Tensor, bias: torch.Tensor, mask: 
     if Y.stride(1) != 1 or I.stride(1) != 1 or I.stride(0) != ldY:
         raise ValueError("Y and I must share a row stride with unit column stride")
     lib = _lib.load()
+    if multicast_out is not None and extra_out:
+        raise ValueError("multicast_out and extra_out are exclusive")
     with torch.cuda.device(H.device):
-        if extra_out:
+        if multicast_out is not None:
+            rc = lib.sparton_fwd_multicast(Hp.data_ptr(), Ep.data_ptr(), bias.data_ptr(), m.data_ptr(),
+                                           int(multicast_out[0]), int(multicast_out[1]), B, S, Dp, V, ldY,
+                                           int(cta_group), _stream_ptr())
+        elif extra_out:
             import ctypes
             n = 1 + len(extra_out)
             ys = (ctypes.c_void_p * n)(Y.data_ptr(), *[int(y) for y, _ in extra_out])

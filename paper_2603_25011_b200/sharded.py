@@ -86,19 +86,37 @@ class FusedVocabGather:
     maps the peers' buffers with CUDA IPC)."""
 
     def __init__(self, Y: torch.Tensor, I: torch.Tensor, peers, barrier: Callable[[int], None],
-                 keepalive=()):
+                 keepalive=(), multicast: tuple[int, int] | None = None):
         if Y.shape != I.shape or Y.dtype != torch.float32 or I.dtype != torch.int32:
             raise ValueError("Y must be float32 and I int32 of the same [B, V] shape")
-        if len(peers) > 7:
+        if len(peers) > 7 and multicast is None:
             raise ValueError("the fused gather addresses at most 8 ranks (sparton_fwd_multi)")
         self.Y, self.I = Y, I
         self.B, self.V = Y.shape
         self.peers = [(int(y), int(i)) for y, i in peers]
+        self.multicast = None if multicast is None else (int(multicast[0]), int(multicast[1]))
         self.barrier = barrier
         self._keepalive = keepalive
 
+    @staticmethod
+    def pick_multicast(hY, hI, multicast: bool | None):
+        """The (Y, I) multicast base addresses to store through, or None for
+        P2P stores.  ``multicast`` None = use NVLS when both symmetric buffers
+        have a multicast mapping (torch reports 0 without NVLS); True =
+        require it; False = P2P stores."""
+        ptrs = (int(getattr(hY, "multicast_ptr", 0) or 0), int(getattr(hI, "multicast_ptr", 0) or 0))
+        have = ptrs[0] != 0 and ptrs[1] != 0
+        if multicast and not have:
+            raise RuntimeError("NVLS multicast requested but the symmetric buffers have no multicast mapping")
+        return ptrs if (have and multicast is not False) else None
+
     @classmethod
-    def symmetric(cls, B: int, V: int, device, group=None) -> "FusedVocabGather":
+    def symmetric(cls, B: int, V: int, device, group=None, multicast: bool | None = False) -> "FusedVocabGather":
+        """``multicast``: store through the NVLS multicast mapping (one
+        multimem.st per result, replicated by the switch) instead of P2P
+        stores to every peer — see ``pick_multicast``.  Off by default: the
+        one-GPU hosts this was built on cannot create a multicast object
+        (tools/nvls_probe.py), so the P2P path is the validated one."""
         import torch.distributed._symmetric_memory as symm_mem
         world, rank = _world(group)
         grp = group if group is not None else dist.group.WORLD
@@ -107,14 +125,19 @@ class FusedVocabGather:
         hY = symm_mem.rendezvous(Y, grp)
         hI = symm_mem.rendezvous(I, grp)
         peers = [(hY.buffer_ptrs[r], hI.buffer_ptrs[r]) for r in range(world) if r != rank]
-        return cls(Y, I, peers, lambda ch: hY.barrier(channel=ch), keepalive=(hY, hI))
+        return cls(Y, I, peers, lambda ch: hY.barrier(channel=ch), keepalive=(hY, hI),
+                   multicast=cls.pick_multicast(hY, hI, multicast))
 
     def forward(self, H, E_shard, bias_shard, mask, v0: int):
         v1 = v0 + E_shard.shape[0]
         if not 0 <= v0 <= v1 <= self.V:
             raise ValueError(f"shard columns [{v0}, {v1}) outside [0, {self.V})")
         self.barrier(0)
-        if v1 > v0:
+        if v1 > v0 and self.multicast is not None:
+            ym, im = self.multicast
+            sparton_forward(H, E_shard, bias_shard, mask, out=(self.Y[:, v0:v1], self.I[:, v0:v1]),
+                            multicast_out=(ym + 4 * v0, im + 4 * v0))
+        elif v1 > v0:
             sparton_forward(H, E_shard, bias_shard, mask, out=(self.Y[:, v0:v1], self.I[:, v0:v1]),
                             extra_out=tuple((y + 4 * v0, i + 4 * v0) for y, i in self.peers))
         self.barrier(1)

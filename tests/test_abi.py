@@ -22,7 +22,8 @@ def _declared():
 def test_header_declares_entry_points():
     names = _declared()
     assert names == sorted(["sparton_abi_version", "sparton_last_error", "sparton_device_sm_count",
-                            "sparton_fwd", "sparton_fwd_fp8", "sparton_fwd_multi", "sparton_quantize_e4m3",
+                            "sparton_fwd", "sparton_fwd_fp8", "sparton_fwd_multi", "sparton_fwd_multicast",
+                            "sparton_quantize_e4m3",
                             "sparton_bwd_workspace_bytes", "sparton_bwd", "sparton_bwd_ex",
                             "sparton_bwd_fp8", "sparton_mx_scales_bytes", "sparton_quantize_mx",
                             "sparton_fwd_mx"])
@@ -84,6 +85,14 @@ def test_fwd_rejects_null_and_misaligned():
     assert lib.sparton_fwd(odd, a, a, a, a, a, 2, 3, 8, 5, 5, 0, None) == _lib.SPARTON_EINVAL
     assert lib.sparton_fwd(a, a, a, a, a, a, 2, 3, 8, 5, 4, 0, None) == _lib.SPARTON_EINVAL  # ldY < V
     assert lib.sparton_fwd(a, a, a, a, a, a, 2, 3, 8, 5, 5, 3, None) == _lib.SPARTON_EINVAL  # cta_group
+
+
+def test_fwd_multicast_rejects_bad_arguments_before_any_cuda_call():
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    a = ctypes.c_void_p(256)
+    assert lib.sparton_fwd_multicast(a, a, a, a, None, a, 2, 3, 8, 5, 5, 0, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_fwd_multicast(a, a, a, a, a, a, 2, 3, 8, 5, 4, 0, None) == _lib.SPARTON_EINVAL  # ldY < V
 
 
 def test_bwd_rejects_small_workspace():

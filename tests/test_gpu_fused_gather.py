@@ -54,6 +54,31 @@ def test_multi_destination_forward(cuda_device, dims):
         assert bool((i[:, :off] == -9).all()) and bool((i[:, off + V:] == -9).all())
 
 
+@pytest.mark.parametrize("dims", [(3, 300, 256, 1000), (5, 17, 64, 300)])
+def test_multicast_store_path_addressing(cuda_device, dims):
+    """The NVLS store path (sparton_fwd_multicast: multimem.st.relaxed.sys,
+    i.e. STG.E.STRONG.SYS to the given address) aimed at an ordinary device
+    buffer: the switch replication needs >= 2 GPUs, but the epilogue's
+    addressing (strided column view, row stride ldY) is checked here — the
+    buffer receives exactly the plain forward's results and nothing outside
+    its columns; the `out` buffer itself is left untouched."""
+    from paper_2603_25011_b200 import sparton_forward
+    B, S, D, V = dims
+    dev = cuda_device
+    H, E, b, m, _ = _inputs(B, S, D, V, dev)
+    Y0, I0 = sparton_forward(H, E, b, m)
+    W, off = V + 29, 13
+    y, i = torch.full((B, W), -7.0, device=dev), torch.full((B, W), -9, dtype=torch.int32, device=dev)
+    oy, oi = torch.full((B, W), -5.0, device=dev), torch.full((B, W), -3, dtype=torch.int32, device=dev)
+    sparton_forward(H, E, b, m, out=(oy[:, off:off + V], oi[:, off:off + V]),
+                    multicast_out=(y[:, off:].data_ptr(), i[:, off:].data_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(y[:, off:off + V], Y0) and torch.equal(i[:, off:off + V], I0)
+    assert bool((y[:, :off] == -7).all()) and bool((y[:, off + V:] == -7).all())
+    assert bool((i[:, :off] == -9).all()) and bool((i[:, off + V:] == -9).all())
+    assert bool((oy == -5).all()) and bool((oi == -3).all())
+
+
 def test_multi_destination_rejects_more_than_eight(cuda_device):
     from paper_2603_25011_b200 import sparton_forward
     H, E, b, m, _ = _inputs(2, 8, 16, 10, cuda_device)

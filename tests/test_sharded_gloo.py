@@ -77,3 +77,19 @@ def test_vocab_sharded_matches_unsharded(dims):
         assert Y.tobytes() == Yr.tobytes() and np.array_equal(I, Ir)
         assert np.allclose(dH, dHr, rtol=1e-5, atol=1e-6)
         assert dE.tobytes() == dEr[v0:v1].tobytes() and db.tobytes() == dbr[v0:v1].tobytes()
+
+
+def test_fused_gather_multicast_selection():
+    """FusedVocabGather.pick_multicast: NVLS only when both symmetric buffers
+    have a multicast mapping (auto), required on request, never when off."""
+    from types import SimpleNamespace as NS
+    from paper_2603_25011_b200.sharded import FusedVocabGather as F
+    with_mc = (NS(multicast_ptr=0x1000), NS(multicast_ptr=0x2000))
+    without = (NS(multicast_ptr=0), NS(multicast_ptr=0x2000))
+    assert F.pick_multicast(*with_mc, None) == (0x1000, 0x2000)
+    assert F.pick_multicast(*with_mc, True) == (0x1000, 0x2000)
+    assert F.pick_multicast(*with_mc, False) is None
+    assert F.pick_multicast(*without, None) is None
+    assert F.pick_multicast(NS(), NS(), None) is None
+    with pytest.raises(RuntimeError):
+        F.pick_multicast(*without, True)
