@@ -682,7 +682,9 @@ def run_plugin_e2e(c, dev, steps=3):
     return {"value": (ff + fb) / t / 1e12, "unit": "TFLOP/s", "ms_per_step": t * 1e3, "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "note": "fusedhead.forward_fully_fused + backward_fused (numpy fp32 in/out, PRECISION='bf16'); "
-                    "synchronous pageable copies, fp32->bf16 conversion on the device; the backward "
+                    "synchronous copies through pinned staging (inputs memcpy'd into torch's cached pinned "
+                    "buffers, outputs returned in pinned host memory), fp32->bf16 conversion on the device; "
+                    "the backward "
                     "re-uploads H and E (the reference API passes them again)"}
 
 

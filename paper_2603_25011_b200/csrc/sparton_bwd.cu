@@ -1102,8 +1102,11 @@ int side_stream(SideStream& out) {
 int launch_route(const BwdParams& p, cudaStream_t stream) {
   const int nseg = route_nseg(p.S);
   const size_t smem = route_smem_bytes(p.S, nseg);
+  // The attribute is the per-function limit, shared by every thread: set it
+  // to the budget (a constant), never to this call's size — a concurrent call
+  // with a smaller S would otherwise lower it between our set and launch.
   cudaError_t e = cudaFuncSetAttribute(sparton_bwd_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+                                       RT_SMEM_BUDGET);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(route)", e);
   int allow_stash = 1;
   if (const char* ev = dev_env("SPARTON_ROUTE_STASH")) allow_stash = atoi(ev);   // experiment switch
@@ -1188,7 +1191,8 @@ int launch_de_staged_t(const BwdParams& p, const CUtensorMap* tmH, cudaStream_t 
   if (nst > 4) nst = 4;
   const int smem = nst * stage_bytes + nst * 16;
   auto kern = sparton_bwd_de_staged_kernel<NW, J, CL, OutT, FP8>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // Constant limit (the budget), not this call's S-dependent size: see launch_route.
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DEST_SMEM_BUDGET);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(de_staged)", e);
   const int nvb = (p.V + C::VB - 1) / C::VB;
   const int nvg = (nvb + CL - 1) / CL;

@@ -101,9 +101,25 @@ def _precision() -> str:
     return PRECISION
 
 
-def _upload(x: np.ndarray, dev, precision: str) -> torch.Tensor:
-    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
-    return t if precision == "fp32" else t.to(torch.bfloat16)
+def _upload(x: np.ndarray, dev, precision: str | None = None, dtype=np.float32) -> torch.Tensor:
+    """Host array -> device tensor through a pinned staging copy (torch's
+    caching host allocator): ~47 GB/s memcpy + ~56 GB/s DMA on the B200 box
+    vs ~11 GB/s for a pageable copy (tools/xfer_probe.py).  bf16 conversion
+    happens on the device."""
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=dtype)).pin_memory().to(dev, non_blocking=True)
+    return t if precision in (None, "fp32") else t.to(torch.bfloat16)
+
+
+def _download(*ts: torch.Tensor) -> list[np.ndarray]:
+    """Device tensors -> numpy arrays backed by pinned host memory (DMA at
+    ~57 GB/s; a fresh pageable ``.cpu()`` runs at ~2.3 GB/s, page faults
+    included).  The arrays keep their pinned blocks alive; freed blocks
+    return to torch's host cache for the next call."""
+    hs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in ts]
+    for h, t in zip(hs, ts):
+        h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in hs]
 
 
 class _Charge:
@@ -146,10 +162,11 @@ def _run_forward(inputs, tracker) -> HeadOutput:
             prec = _precision()
             H = _upload(inputs.H, dev, prec)
             E = _upload(inputs.E, dev, prec)
-            b = torch.from_numpy(np.ascontiguousarray(inputs.b, dtype=np.float32)).to(dev)
-            m = torch.from_numpy(np.ascontiguousarray(inputs.mask, dtype=np.uint8)).to(dev)
+            b = _upload(inputs.b, dev)
+            m = _upload(inputs.mask, dev, dtype=np.uint8)
             Y, I = (sparton_forward_fp32 if prec == "fp32" else sparton_forward)(H, E, b, m)
-            out = HeadOutput(Y=Y.cpu().numpy(), I=I.cpu().numpy())
+            Yh, Ih = _download(Y, I)
+            out = HeadOutput(Y=Yh, I=Ih)
         except torch.OutOfMemoryError as exc:
             raise _device_oom(tracker, nbytes, exc) from exc
     if tracker is not None:
@@ -188,12 +205,13 @@ def backward_fused(inputs, saved, dY: np.ndarray, cfg=None, *,
     prec = _precision()
     H = _upload(inputs.H, dev, prec)
     E = _upload(inputs.E, dev, prec)
-    Y = torch.from_numpy(np.ascontiguousarray(saved.Y, dtype=np.float32)).to(dev)
-    I = torch.from_numpy(np.ascontiguousarray(saved.I, dtype=np.int32)).to(dev)
-    g = torch.from_numpy(np.ascontiguousarray(dY, dtype=np.float32)).to(dev)
+    Y = _upload(saved.Y, dev)
+    I = _upload(saved.I, dev, dtype=np.int32)
+    g = _upload(dY, dev)
     bwd = sparton_backward_fp32 if prec == "fp32" else sparton_backward
     dH, dE, db = bwd(H, E, Y, I, g, include_bias_grad=include_bias_grad)
-    return HeadGradients(dH=dH.cpu().numpy(), dE=dE.cpu().numpy(), db=db.cpu().numpy())
+    dHh, dEh, dbh = _download(dH, dE, db)
+    return HeadGradients(dH=dHh, dE=dEh, db=dbh)
 
 
 def run_b200(inputs, cfg, tracker) -> HeadOutput:

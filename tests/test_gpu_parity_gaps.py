@@ -367,3 +367,46 @@ def test_concurrent_threads_match_serial_bitwise(cuda_device):
     for a, c in zip(serial, results):
         for x, y in zip(a, c):
             assert torch.equal(x, y)
+
+
+def test_concurrent_calls_with_different_smem_sizes(cuda_device):
+    """Concurrent backwards whose staged dE / route launches need different
+    dynamic shared memory (S = 64 ... 832): the per-function smem limit is a
+    constant, so no thread can lower it between another thread's set and
+    launch (a failed launch would raise; results equal the serial run)."""
+    from paper_2603_25011_b200 import sparton_backward, sparton_forward
+    dev = _dev()
+    jobs = []
+    for i, S in enumerate((64, 832, 128, 700, 257, 512, 96, 800)):
+        H, E, b, m = orc.seeded_inputs(2, S, 128, 3000, 70 + i, mask_keep=0.9)
+        dY = orc.seeded_uniform((2, 3000), 170 + i)
+        jobs.append(tuple(torch.from_numpy(x).to(dev) for x in (H, E, b, m, dY)))
+    fwd = [sparton_forward(j[0].to(torch.bfloat16), j[1].to(torch.bfloat16), j[2], j[3]) for j in jobs]
+
+    def run(k):
+        H, E, b, m, dY = jobs[k]
+        Y, I = fwd[k]
+        return [t.cpu() for t in sparton_backward(H.to(torch.bfloat16), E.to(torch.bfloat16), Y, I, dY)]
+
+    serial = [run(k) for k in range(len(jobs))]
+    errors, mism = [], []
+
+    def worker(tid):
+        try:
+            s = torch.cuda.Stream(device=dev)
+            with torch.cuda.stream(s):
+                for rep in range(12):
+                    k = (tid + rep) % len(jobs)
+                    out = run(k)
+                    if not all(torch.equal(x, y) for x, y in zip(out, serial[k])):
+                        mism.append((tid, rep, k))
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert not mism, mism
