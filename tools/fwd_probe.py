@@ -10,7 +10,7 @@ H = torch.randn((B, S, D), device=dev).to(torch.bfloat16)
 E = (torch.randn((V, D), device=dev) * 0.02).to(torch.bfloat16)
 b = torch.zeros(V, device=dev)
 m = torch.ones((B, S), dtype=torch.uint8, device=dev)
-for _ in range(2):
+for _ in range(int(sys.argv[5]) if len(sys.argv) > 5 else 2):
     Y, I = sparton_forward(H, E, b, m)
 torch.cuda.synchronize()
 print("ok", float(Y.sum()))
