@@ -1,9 +1,10 @@
-"""A/B two builds of libsparton_b200.so on the cfg3 fwd+bwd step, in ONE
-process on one box (alternating A B A B ... to cancel clock drift).  Uses only
-the entry points every build exports (sparton_fwd, sparton_bwd, workspace
-query) through ctypes, so builds from earlier rounds can be compared.
+"""A/B two or more builds of libsparton_b200.so on the cfg3 fwd+bwd step, in
+ONE process on one box (alternating A B ... A B ... to cancel clock drift).
+Uses only the entry points every build exports (sparton_fwd, sparton_bwd,
+workspace query) through ctypes, so builds from earlier rounds can be compared;
+checks that every build produces the same Y, I, dH, dE and db.
 
-    python tools/ab_step.py build/ab/r01.so build/ab/cur.so [rounds] [steps]
+    python tools/ab_step.py build/ab/r01.so build/ab/cur.so [more.so ...] [--rounds 4] [--steps 10]
 """
 import ctypes
 import statistics
@@ -11,9 +12,15 @@ import sys
 
 import torch
 
-libs = [ctypes.CDLL(p) for p in sys.argv[1:3]]
-rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 4
-steps = int(sys.argv[4]) if len(sys.argv) > 4 else 10
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("libs", nargs="+")
+ap.add_argument("--rounds", type=int, default=4)
+ap.add_argument("--steps", type=int, default=10)
+args = ap.parse_args()
+names = args.libs
+libs = [ctypes.CDLL(p) for p in names]
+rounds, steps = args.rounds, args.steps
 vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
 for lib in libs:
     lib.sparton_fwd.argtypes = [vp] * 6 + [i64] * 5 + [ci, vp]
@@ -50,13 +57,21 @@ def step(lib, fwd_ev):
                            dE.data_ptr(), db.data_ptr(), B, S, D, V, V, V, 1, 1, ws.data_ptr(), ws_n, st) == 0
 
 
-res = {0: [], 1: []}
+res = {k: [] for k in range(len(libs))}
+ref = None
 for r in range(rounds):
     for k, lib in enumerate(libs):
         fe = []
         for _ in range(3):
             step(lib, fe)
         torch.cuda.synchronize()
+        if r == 0:   # every build must compute the same outputs
+            out = [t.clone() for t in (Y, I, dH, dE, db)]
+            if ref is None:
+                ref = out
+            else:
+                same = [torch.equal(a, c) for a, c in zip(ref, out)]
+                print(f"{names[k]}: outputs equal to {names[0]} (Y, I, dH, dE, db): {same}", flush=True)
         fe.clear()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
@@ -67,8 +82,8 @@ for r in range(rounds):
         ms = t0.elapsed_time(t1) / steps
         fwd = statistics.mean(a.elapsed_time(c) for a, c in fe)
         res[k].append((ms, fwd))
-        print(f"round {r} {sys.argv[1 + k]}: step {ms:.2f} ms  fwd {fwd:.2f}  bwd {ms - fwd:.2f}", flush=True)
-for k in (0, 1):
+        print(f"round {r} {names[k]}: step {ms:.2f} ms  fwd {fwd:.2f}  bwd {ms - fwd:.2f}", flush=True)
+for k in range(len(libs)):
     ms = statistics.median(x[0] for x in res[k])
     fwd = statistics.median(x[1] for x in res[k])
-    print(f"MEDIAN {sys.argv[1 + k]}: step {ms:.2f} fwd {fwd:.2f} bwd {ms - fwd:.2f}")
+    print(f"MEDIAN {names[k]}: step {ms:.2f} fwd {fwd:.2f} bwd {ms - fwd:.2f}")
