@@ -513,6 +513,8 @@ def run_gpu_arm(args, c, cname):
                         "gpu_launches": launches_per_step(c4, -(-c4["V"] // world)) * args.steps * world}
     if world == 1 and cname != "cfg1" and not args.no_cfg1:
         line["cfg1"] = gpu_cfg1(dev, args.steps, args.warmup)
+    if world == 1 and not args.no_naive:
+        line["naive_pytorch"] = naive_pytorch(c, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         arm = CpuArm(c)
         line["cpu_baseline"] = arm.describe(arm.sample())
@@ -522,6 +524,53 @@ def run_gpu_arm(args, c, cname):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def naive_pytorch(c, dev, steps=2):
+    """The naive PyTorch GPU head on the same box (north_star):
+    ``((H @ E.T + b) * M).relu().log1p().max(dim=1)`` with autograd, bf16,
+    fwd + bwd per step, CUDA events.  It materialises the B×S×V logits, so at
+    cfg3 it runs out of the 180 GB: the record keeps the OOM and times the
+    largest batch (halving B) that fits, with the same algorithmic-FLOP
+    accounting as the fused head."""
+    import torch
+
+    def step(H, E, b, m, dY):
+        Hq, Eq, bq = (t.detach().requires_grad_(True) for t in (H, E, b))
+        L = (torch.einsum("bsd,vd->bsv", Hq, Eq) + bq.to(Hq.dtype)) * m[..., None].to(Hq.dtype)
+        Y = L.relu().log1p().max(dim=1).values.float()
+        Y.backward(dY)
+
+    rec = {"formula": "((H@E.T + b) * M).relu().log1p().max(dim=1), torch autograd, bf16", "oom_at_B": []}
+    B = c["B"]
+    while B >= 1:
+        cb = dict(c, B=B)
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats(dev)
+        base = torch.cuda.memory_allocated(dev)
+        try:
+            H, E, b, m, dY, _ = make_inputs(cb, dev, 0, 1)
+            step(H, E, b, m, dY)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                step(H, E, b, m, dY)
+            e1.record()
+            torch.cuda.synchronize()
+        except torch.OutOfMemoryError:
+            rec["oom_at_B"].append(B)
+            H = E = b = m = dY = None
+            B //= 2
+            continue
+        ms = e0.elapsed_time(e1) / steps
+        ff, fb = flops(cb)
+        rec.update({"B": B, "ms_per_step": ms, "value": (ff + fb) / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                    "steps": steps, "peak_hbm_bytes": torch.cuda.max_memory_allocated(dev) - base})
+        del H, E, b, m, dY
+        break
+    torch.cuda.empty_cache()
+    return rec
 
 
 def gpu_cfg1(dev, steps, warmup):
@@ -701,6 +750,7 @@ def main() -> int:
     ap.add_argument("--no-fused-ab", action="store_true", help="N>1: skip the fused all-gather A/B record")
     ap.add_argument("--no-sparse", action="store_true", help="N=1: skip the SPLADE-sparse (bias -2) record")
     ap.add_argument("--no-cfg1", action="store_true", help="N=1: skip the cfg1 (reference CPU case) record")
+    ap.add_argument("--no-naive", action="store_true", help="N=1: skip the naive PyTorch head record")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":

@@ -3,8 +3,8 @@
 # `ncu --set full` capture per kernel family (cfg3), then bench lines.
 # Summaries: python tools/make_profiles.py <tag>
 mkdir -p gpurun_out
-B="timeout 600 python bench.py --steps 1 --warmup 1 --no-cpu --no-plugin --no-sparse --no-cfg1"
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none --csv --log-file gpurun_out/launches_cfg3.csv timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu --no-plugin --no-sparse --no-cfg1 > /dev/null 2>&1
+B="timeout 600 python bench.py --steps 1 --warmup 1 --no-cpu --no-plugin --no-sparse --no-cfg1 --no-naive"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none --csv --log-file gpurun_out/launches_cfg3.csv timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu --no-plugin --no-sparse --no-cfg1 --no-naive > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sparton_fwd -s 1 -c 1 -f -o gpurun_out/full_fwd $B > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sparton_bwd_de_staged -s 1 -c 1 -f -o gpurun_out/full_de $B > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sparton_bwd_route -s 1 -c 1 -f -o gpurun_out/full_route $B > /dev/null 2>&1
