@@ -96,14 +96,15 @@ def measured_peaks():
     return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
 
 
-def ncu_traffic(config_name):
-    """DRAM bytes per forward launch from the committed ncu capture, if any."""
+def ncu_fwd(config_name, key="dram_bytes"):
+    """A per-launch figure of the forward from the committed ncu capture
+    (profiles/ncu_summary.json, tools/make_profiles.py), if any."""
     p = REPO / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get("fwd", {}).get(config_name, {}).get("dram_bytes")
+        return d.get("fwd", {}).get(config_name, {}).get(key)
     except Exception:
         return None
 
@@ -446,7 +447,8 @@ def run_gpu_arm(args, c, cname):
                      "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                      "frac": achieved / peaks["bf16_tflops_sustained"],
                      "frac_of_burst": achieved / peaks["bf16_tflops"],
-                     "traffic": ncu_traffic(cname), "algorithmic_flops_per_launch": fwd_flops_rank,
+                     "traffic": ncu_fwd(cname), "algorithmic_flops_per_launch": fwd_flops_rank,
+                     "ncu_tensor_pipe_pct": ncu_fwd(cname, "tensor_pipe_pct"),
                      "peak_source": peaks["source"] + " (sustained: K1 runs inside a long step; burst in "
                                     "frac_of_burst. frac > 1 means the step's lighter backward phase lets the "
                                     "forward hold higher clocks than a back-to-back cuBLAS loop at the power cap)"},
