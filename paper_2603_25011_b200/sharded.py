@@ -57,6 +57,15 @@ def gather_vocab(Y_p: torch.Tensor, I_p: torch.Tensor, V: int, Vp: int, group=No
     Ib = torch.zeros((B, Vp), dtype=I_p.dtype, device=I_p.device)
     Yb[:, :n] = Y_p
     Ib[:, :n] = I_p
+    if _flat_collectives(group, Y_p):
+        # One [P, B, Vp] buffer per output, then one permute copy to [B, V].
+        ys = torch.empty((world * B, Vp), dtype=Y_p.dtype, device=Y_p.device)
+        is_ = torch.empty((world * B, Vp), dtype=I_p.dtype, device=I_p.device)
+        dist.all_gather_into_tensor(ys, Yb, group=group)
+        dist.all_gather_into_tensor(is_, Ib, group=group)
+        Y = ys.view(world, B, Vp).permute(1, 0, 2).reshape(B, world * Vp)[:, :V].contiguous()
+        I = is_.view(world, B, Vp).permute(1, 0, 2).reshape(B, world * Vp)[:, :V].contiguous()
+        return Y, I
     ys = [torch.empty_like(Yb) for _ in range(world)]
     is_ = [torch.empty_like(Ib) for _ in range(world)]
     dist.all_gather(ys, Yb, group=group)
@@ -64,6 +73,35 @@ def gather_vocab(Y_p: torch.Tensor, I_p: torch.Tensor, V: int, Vp: int, group=No
     Y = torch.cat(ys, dim=1)[:, :V].contiguous()
     I = torch.cat(is_, dim=1)[:, :V].contiguous()
     return Y, I
+
+
+def _flat_collectives(group, t: torch.Tensor) -> bool:
+    """NCCL (or any backend on CPU tensors) takes the flat tensor collectives
+    (all_gather_into_tensor / reduce_scatter_tensor); gloo with CUDA tensors
+    (the one-GPU multi-rank tests) keeps the list / all-reduce forms."""
+    return not t.is_cuda or dist.get_backend(group) == "nccl"
+
+
+def reduce_dh(dH: torch.Tensor, grad_dtype: torch.dtype, group=None) -> torch.Tensor:
+    """Sum the per-rank partial dH (fp32) over the group and return it in
+    ``grad_dtype``.  For a narrower ``grad_dtype`` the sum is a reduce-scatter
+    in fp32 (the reference's accumulation precision), the cast of each rank's
+    reduced rows, and an all-gather of the cast rows: the same values as an
+    fp32 all-reduce followed by the cast, with 2/3 of its bytes on the wire
+    for bf16 (fp32 reduce-scatter + bf16 all-gather vs two fp32 phases)."""
+    world, _ = _world(group)
+    if world == 1:
+        return dH if grad_dtype == torch.float32 else dH.to(grad_dtype)
+    n = dH.numel()
+    if grad_dtype != torch.float32 and n % world == 0 and _flat_collectives(group, dH):
+        flat = dH.reshape(-1)
+        part = torch.empty(n // world, dtype=torch.float32, device=dH.device)
+        dist.reduce_scatter_tensor(part, flat, op=dist.ReduceOp.SUM, group=group)
+        out = torch.empty(n, dtype=grad_dtype, device=dH.device)
+        dist.all_gather_into_tensor(out, part.to(grad_dtype), group=group)
+        return out.view(dH.shape)
+    dist.all_reduce(dH, op=dist.ReduceOp.SUM, group=group)
+    return dH if grad_dtype == torch.float32 else dH.to(grad_dtype)
 
 
 class FusedVocabGather:
@@ -153,27 +191,27 @@ def local_backward(H, E_shard, Y_p, I_p, dY_p, *, grad_dtype=torch.float32, incl
     backward, the all-reduce runs on its own stream as soon as dH is final
     (``dh_ready`` event) and overlaps the shard's dE, which the library runs
     on a side stream; the caller's stream waits for both.  The reduction is
-    in fp32 (the reference accumulates in fp32), then cast to ``grad_dtype``."""
+    in fp32 (the reference accumulates in fp32), then cast to ``grad_dtype``
+    (``reduce_dh``: reduce-scatter, cast, all-gather for a bf16 result)."""
     world, _ = _world(group)
     if local_bwd is not None or not H.is_cuda or world == 1:
         fn = local_bwd or sparton_backward
         dH, dE, db = fn(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
                         grad_dtype=torch.float32)
-        if world > 1:
-            dist.all_reduce(dH, op=dist.ReduceOp.SUM, group=group)
+        dH = reduce_dh(dH, grad_dtype, group)
     else:
         main = torch.cuda.current_stream(H.device)
         ready = torch.cuda.Event()
-        dH, dE, db = sparton_backward(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
-                                      grad_dtype=torch.float32, dh_ready=ready)
+        dH32, dE, db = sparton_backward(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
+                                        grad_dtype=torch.float32, dh_ready=ready)
         comm = _comm_stream(H.device)
         comm.wait_event(ready)
         with torch.cuda.stream(comm):
-            dist.all_reduce(dH, op=dist.ReduceOp.SUM, group=group)
+            dH = reduce_dh(dH32, grad_dtype, group)
+        dH32.record_stream(comm)
         dH.record_stream(comm)
         main.wait_stream(comm)
     if grad_dtype != torch.float32:
-        dH = dH.to(grad_dtype)
         dE = dE.to(grad_dtype)
     return dH, dE, db
 

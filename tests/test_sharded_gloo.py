@@ -93,3 +93,43 @@ def test_fused_gather_multicast_selection():
     assert F.pick_multicast(NS(), NS(), None) is None
     with pytest.raises(RuntimeError):
         F.pick_multicast(*without, True)
+
+
+def _reduce_worker(rank, world, port, shape, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_25011_b200.sharded import reduce_dh
+        g = torch.Generator().manual_seed(100 + rank)
+        part = torch.randn(shape, generator=g)
+        ref = part.clone()
+        dist.all_reduce(ref)
+        out = {}
+        for dt in (torch.bfloat16, torch.float32):
+            r = reduce_dh(part.clone(), dt)
+            out[str(dt)] = (r.dtype == dt, tuple(r.shape) == shape, torch.equal(r, ref.to(dt)))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape", [(2, 6, 8), (3, 5, 7)])   # divisible by the world size / not (all-reduce fallback)
+def test_reduce_dh_matches_fp32_allreduce_then_cast(shape):
+    """sharded.reduce_dh: the bf16 result of the fp32 reduce-scatter + bf16
+    all-gather equals an fp32 all-reduce followed by the cast (two ranks:
+    the fp32 sums are order-independent), for both the flat path and the
+    all-reduce fallback; fp32 stays an fp32 all-reduce."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reduce_worker, args=(r, world, port, shape, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, out in res:
+        for dt, checks in out.items():
+            assert all(checks), (rank, dt, checks)
