@@ -30,12 +30,12 @@ from oracle import sparton_oracle as orc
 pytestmark = pytest.mark.gpu
 
 
-def _inputs(B, S, D, V, bias_std, keep, seed):
+def _inputs(B, S, D, V, bias_std, keep, seed, bias_mean=0.0):
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(seed)
     H = torch.randn((B, S, D), generator=g, device=dev).to(torch.bfloat16)
     E = (torch.randn((V, D), generator=g, device=dev) * 0.02).to(torch.bfloat16)
-    b = torch.randn(V, generator=g, device=dev) * bias_std
+    b = torch.randn(V, generator=g, device=dev) * bias_std + bias_mean
     m = (torch.rand((B, S), generator=g, device=dev) < keep).to(torch.uint8)
     m[:, 0] = 1
     dY = torch.randn((B, V), generator=g, device=dev)
@@ -105,15 +105,19 @@ def _close(a, b, rtol, atol):
     return int(bad.sum()), float((a - b).abs().max())
 
 
-@pytest.mark.parametrize("name,dims,bias_std,keep", [
-    ("cfg2_bias_ragged", (512, 512, 768, 30522), 0.1, 0.9),
-    ("cfg3_bench", (512, 512, 768, 250002), 0.0, 1.0),
-    ("cfg4_shape", (2048, 512, 1024, 250002), 0.05, 0.95),
+@pytest.mark.parametrize("name,dims,bias_std,keep,bias_mean", [
+    ("cfg2_bias_ragged", (512, 512, 768, 30522), 0.1, 0.9, 0.0),
+    ("cfg3_bench", (512, 512, 768, 250002), 0.0, 1.0, 0.0),
+    ("cfg4_shape", (2048, 512, 1024, 250002), 0.05, 0.95, 0.0),
+    # SPLADE-sparse inputs: bias -2 leaves a few % of the pairs
+    # active, so the backward takes its sparse-regime kernels (per-pair dE
+    # gathers, single-pass dH).
+    ("cfg3_sparse", (512, 512, 768, 250002), 0.0, 1.0, -2.0),
 ])
-def test_fullsize_forward_backward_vs_torch_fp32(cuda_device, name, dims, bias_std, keep):
+def test_fullsize_forward_backward_vs_torch_fp32(cuda_device, name, dims, bias_std, keep, bias_mean):
     from paper_2603_25011_b200 import sparton_backward, sparton_forward
     B, S, D, V = dims
-    H, E, b, m, dY = _inputs(B, S, D, V, bias_std, keep, seed=7)
+    H, E, b, m, dY = _inputs(B, S, D, V, bias_std, keep, seed=7, bias_mean=bias_mean)
     Y, I = sparton_forward(H, E, b, m)
     dHb, dEb, dbb = sparton_backward(H, E, Y, I, dY, grad_dtype=torch.bfloat16)
     dHf, dEf, dbf = sparton_backward(H, E, Y, I, dY, grad_dtype=torch.float32)
@@ -134,4 +138,6 @@ def test_fullsize_forward_backward_vs_torch_fp32(cuda_device, name, dims, bias_s
                                       ("db f32", dbf, dbr, 1e-4, 1e-4)):
         nbad, dmax = _close(got.float(), ref, rtol, atol)
         assert nbad == 0, f"{name} {tag}: {nbad} elements outside tolerance (max abs diff {dmax})"
-    print(f"{name}: {B * V} (Y, I) pairs, {n_mism} argmax differences, all certified near-ties")
+    act = float((Y > 0).float().mean())
+    print(f"{name}: {B * V} (Y, I) pairs ({100 * act:.1f} % active), {n_mism} argmax differences, "
+          "all certified near-ties")
