@@ -342,7 +342,8 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False, bi
     ``fused``: N > 1 with the (Y, I) all-gather fused into K1's epilogue
     (sharded.FusedVocabGather) instead of NCCL all-gather + permute copy:
     "p2p" stores to every peer's buffer, "nvls" one multimem store per result
-    through the multicast mapping."""
+    through the multicast mapping; the partial dH is then summed by one kernel
+    over peer memory (sharded.PeerDHReduce: P2P loads/stores, or multimem)."""
     import torch
     import torch.distributed as dist
     from paper_2603_25011_b200 import sharded, sparton_backward, sparton_forward
@@ -352,6 +353,10 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False, bi
     stream = torch.cuda.current_stream()
     fwd_ev = [] if fwd_ev is None else fwd_ev
     fg = sharded.FusedVocabGather.symmetric(c["B"], V, dev, multicast=(fused == "nvls")) if fused else None
+    # The fused runs also reduce dH in one kernel over peer memory (P2P loads
+    # and stores, or multimem.ld_reduce / multimem.st) instead of NCCL.
+    dr = (sharded.PeerDHReduce.symmetric((c["B"], c["S"], c["D"]), torch.bfloat16, dev,
+                                         multicast=(fused == "nvls")) if fused else None)
 
     def step(timed=False):
         if timed:
@@ -370,7 +375,7 @@ def timed_steps(c, dev, rank, world, steps, warmup, fwd_ev=None, fused=False, bi
         else:
             if fg is None:
                 Yg, Ig = sharded.gather_vocab(Y, I, V, Vp)
-            g = sharded.local_backward(H, E, Y, I, dY[:, v0:v1], grad_dtype=torch.bfloat16)
+            g = sharded.local_backward(H, E, Y, I, dY[:, v0:v1], grad_dtype=torch.bfloat16, dh_reduce=dr)
         return Y, I, g
 
     for _ in range(warmup):
@@ -472,7 +477,8 @@ def run_gpu_arm(args, c, cname):
             del inpf
             line["fused_gather"] = {"ms_per_step": msf, "fwd_ms": fwdf, "value": (ff + fb) / (msf * 1e-3) / 1e12,
                                     "unit": "TFLOP/s", "note": "K1 epilogue stores into every rank's symmetric "
-                                    "[B, V] buffers (sparton_fwd_multi) instead of NCCL all-gather"}
+                                    "[B, V] buffers (sparton_fwd_multi) instead of NCCL all-gather; dH "
+                                    "summed by sparton_allreduce_peers (P2P) instead of NCCL"}
         except Exception as exc:
             line["fused_gather"] = {"unavailable": repr(exc)[:300]}
         torch.cuda.empty_cache()
@@ -482,7 +488,8 @@ def run_gpu_arm(args, c, cname):
             line["nvls_gather"] = {"ms_per_step": msn, "fwd_ms": fwdn, "value": (ff + fb) / (msn * 1e-3) / 1e12,
                                    "unit": "TFLOP/s", "note": "K1 epilogue stores each result once with "
                                    "multimem.st to the symmetric buffers' NVLS multicast mapping "
-                                   "(sparton_fwd_multicast)"}
+                                   "(sparton_fwd_multicast); dH summed by multimem.ld_reduce + "
+                                   "multimem.st (sparton_allreduce_multimem)"}
         except Exception as exc:
             line["nvls_gather"] = {"unavailable": repr(exc)[:300]}
         torch.cuda.empty_cache()

@@ -206,6 +206,33 @@ SPARTON_API int sparton_bwd_fp8(const void* H8, const void* E8, const float* ama
                 int include_bias_grad, int grad_dtype,
                 void* workspace, size_t workspace_bytes, void* stream, void* dh_ready_event);
 
+/*
+ * dH reduction of the vocab-sharded head over NVLink peer memory (SURVEY.md
+ * §8e C2): every rank's partial dH (fp32, n elements, n % 4 == 0, 16-B
+ * aligned) sits in a buffer all ranks can address.  After the caller's
+ * barrier (all partials written), rank `rank` sums its slice of float4 units
+ * [rank*c, (rank+1)*c), c = ceil(n/4 / nranks), over the nranks partials in
+ * rank order 0..nranks-1 (deterministic, identical on every rank) and stores
+ * it to every rank's output buffer — fp32, or bf16 rounded once
+ * (out_dtype SPARTON_F32 / SPARTON_BF16); the caller's second barrier
+ * publishes the outputs.  The bytes of a reduce-scatter + all-gather in one
+ * launch.  parts / outs: host arrays of nranks (1..8) device pointers in rank
+ * order (peer-mapped: torch symmetric memory or CUDA IPC).  Replaces no
+ * reference function (the reference has no multi-device path).
+ */
+SPARTON_API int sparton_allreduce_peers(const float* const* parts, void* const* outs, int nranks, int rank,
+                                        int out_dtype, int64_t n, void* stream);
+
+/*
+ * The same reduction through NVLink SHARP: one multimem.ld_reduce.add.v4.f32
+ * per unit on mc_part (the multicast address of the partial buffers — the
+ * switch sums the copies) and one multimem.st to mc_out (the multicast
+ * address of the output buffers).  Needs an NVLS-capable NVSwitch system
+ * (a multicast object of >= 2 GPUs).
+ */
+SPARTON_API int sparton_allreduce_multimem(const float* mc_part, void* mc_out, int nranks, int rank,
+                                           int out_dtype, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,8 @@ EXPORTED = (
     "sparton_mx_scales_bytes",
     "sparton_quantize_mx",
     "sparton_fwd_mx",
+    "sparton_allreduce_peers",
+    "sparton_allreduce_multimem",
 )
 
 _lock = threading.Lock()
@@ -110,6 +112,11 @@ def load() -> ctypes.CDLL:
         lib.sparton_fwd_mx.argtypes = [c_vp] * 8 + [c_i64] * 5 + [c_vp]
         lib.sparton_bwd_fp8.restype = c_int
         lib.sparton_bwd_fp8.argtypes = [c_vp] * 10 + [c_i64] * 6 + [c_int, c_int, c_vp, ctypes.c_size_t, c_vp, c_vp]
+        lib.sparton_allreduce_peers.restype = c_int
+        lib.sparton_allreduce_peers.argtypes = [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_int, c_int, c_int,
+                                                c_i64, c_vp]
+        lib.sparton_allreduce_multimem.restype = c_int
+        lib.sparton_allreduce_multimem.argtypes = [c_vp, c_vp, c_int, c_int, c_int, c_i64, c_vp]
         _lib = lib
         return lib
 

@@ -20,7 +20,7 @@ CSRC = PKG_DIR / "csrc"
 LIB_NAME = "libsparton_b200.so"
 LIB_PATH = PKG_DIR / LIB_NAME
 
-SOURCES = ["sparton_abi.cu", "sparton_fwd.cu", "sparton_bwd.cu"]
+SOURCES = ["sparton_abi.cu", "sparton_fwd.cu", "sparton_bwd.cu", "sparton_coll.cu"]
 HEADERS = ["ptx.cuh", "sparton_internal.h"]
 
 NVCC_FLAGS = [

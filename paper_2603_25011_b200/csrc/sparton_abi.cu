@@ -328,6 +328,44 @@ int sparton_fwd_mx(const void* Hq, const void* Hsf, const void* Eq, const void* 
                     Hsf, Esf);
 }
 
+namespace {
+int check_allreduce(int nranks, int rank, int out_dtype, int64_t n) {
+  if (nranks < 1 || nranks > kMaxPeers) return set_error(SPARTON_EINVAL, "nranks must lie in [1, 8]");
+  if (rank < 0 || rank >= nranks) return set_error(SPARTON_EINVAL, "rank must lie in [0, nranks)");
+  if (out_dtype != SPARTON_F32 && out_dtype != SPARTON_BF16)
+    return set_error(SPARTON_EINVAL, "out_dtype must be SPARTON_F32 or SPARTON_BF16");
+  if (n < 0 || n % 4 != 0) return set_error(SPARTON_EINVAL, "n must be a non-negative multiple of 4");
+  return SPARTON_OK;
+}
+}  // namespace
+
+int sparton_allreduce_peers(const float* const* parts, void* const* outs, int nranks, int rank, int out_dtype,
+                            int64_t n, void* stream) {
+  int rc = check_allreduce(nranks, rank, out_dtype, n);
+  if (rc) return rc;
+  if (!parts || !outs) return set_error(SPARTON_EINVAL, "null pointer array");
+  for (int q = 0; q < nranks; ++q) {
+    if (!parts[q] || !outs[q]) return set_error(SPARTON_EINVAL, "null peer pointer");
+    if (!aligned16(parts[q]) || (reinterpret_cast<uintptr_t>(outs[q]) & (out_dtype == SPARTON_BF16 ? 7u : 15u)))
+      return set_error(SPARTON_EINVAL, "partials must be 16-B aligned, outputs 16-B (fp32) / 8-B (bf16) aligned");
+  }
+  if ((rc = check_device())) return rc;
+  return launch_allreduce_peers(parts, outs, nranks, rank, out_dtype == SPARTON_BF16, n,
+                                static_cast<cudaStream_t>(stream));
+}
+
+int sparton_allreduce_multimem(const float* mc_part, void* mc_out, int nranks, int rank, int out_dtype, int64_t n,
+                               void* stream) {
+  int rc = check_allreduce(nranks, rank, out_dtype, n);
+  if (rc) return rc;
+  if (!mc_part || !mc_out) return set_error(SPARTON_EINVAL, "null multicast address");
+  if (!aligned16(mc_part) || (reinterpret_cast<uintptr_t>(mc_out) & (out_dtype == SPARTON_BF16 ? 7u : 15u)))
+    return set_error(SPARTON_EINVAL, "multicast addresses must be 16-B (fp32) / 8-B (bf16) aligned");
+  if ((rc = check_device())) return rc;
+  return launch_allreduce_multimem(mc_part, mc_out, nranks, rank, out_dtype == SPARTON_BF16, n,
+                                   static_cast<cudaStream_t>(stream));
+}
+
 int sparton_quantize_e4m3(const void* x, int64_t n, void* q, float* amax, void* stream) {
   if (n < 1) return set_error(SPARTON_EINVAL, "n must be positive");
   if (!x || !q || !amax) return set_error(SPARTON_EINVAL, "null pointer argument");

@@ -12,6 +12,7 @@
 namespace sparton {
 
 constexpr int kMaxFwdDst = 8;
+constexpr int kMaxPeers = 8;   // ranks a peer-memory dH reduction addresses (sparton_coll.cu)
 // Sparse-regime thresholds of the backward (percent of the B*V pairs active).
 constexpr double kDeSparsePct = 40.0;
 constexpr double kDhSparsePct = 12.0;
@@ -132,5 +133,11 @@ int encode_u8_2d_plain(CUtensorMap* map, const void* ptr, long long rows, long l
 // Rows of H each CTA of a staged-dE cluster loads per batch row (0: staged dE unsupported for S).
 int de_staged_rows(int S);
 int bwd_max_seq();
+// dH reduction over peer memory (sparton_coll.cu): parts/outs are nranks
+// device pointers in rank order; n fp32 elements, a multiple of 4.
+int launch_allreduce_peers(const float* const* parts, void* const* outs, int nranks, int rank, bool bf16,
+                           long long n, cudaStream_t stream);
+int launch_allreduce_multimem(const float* mc_part, void* mc_out, int nranks, int rank, bool bf16, long long n,
+                              cudaStream_t stream);
 
 }  // namespace sparton

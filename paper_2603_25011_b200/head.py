@@ -352,7 +352,8 @@ def bwd_workspace_bytes(B: int, S: int, D: int, V: int, grad_dtype: torch.dtype 
 def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch.Tensor,
                      dY: torch.Tensor, *, include_bias_grad: bool = True,
                      grad_dtype: torch.dtype = torch.float32,
-                     dh_ready: torch.cuda.Event | None = None
+                     dh_ready: torch.cuda.Event | None = None,
+                     out_dH: torch.Tensor | None = None
                      ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """Argmax-routed backward from the saved (Y, I) only (fused.py:215-278).
 
@@ -363,7 +364,9 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     row-major tensors (unit column stride; row strides passed as ldDY / ldY,
     no copy).  ``dh_ready``, if
     given, is recorded on the current stream as soon as dH is final, before
-    the dE work joins (``sparton_bwd_ex``).
+    the dE work joins (``sparton_bwd_ex``).  ``out_dH`` receives dH instead of
+    a fresh tensor (contiguous [B, S, D] in ``grad_dtype``, D a multiple of 8:
+    e.g. a peer-addressable buffer the sharded head reduces in place).
     """
     for name, t in (("H", H), ("E", E), ("Y", Y), ("I", I), ("dY", dY)):
         _require_cuda(name, t)
@@ -388,7 +391,13 @@ def sparton_backward(H: torch.Tensor, E: torch.Tensor, Y: torch.Tensor, I: torch
     if dY.stride(1) != 1 or dY.stride(0) < V:
         dY = dY.contiguous()
     dev = H.device
-    dH = torch.empty((B, S, Dp), dtype=grad_dtype, device=dev)
+    if out_dH is not None:
+        if (out_dH.shape != (B, S, Dp) or out_dH.dtype != grad_dtype or not out_dH.is_contiguous()
+                or out_dH.device != dev):
+            raise ValueError(f"out_dH must be a contiguous {grad_dtype} tensor of shape {(B, S, Dp)} on {dev}")
+        dH = out_dH
+    else:
+        dH = torch.empty((B, S, Dp), dtype=grad_dtype, device=dev)
     dE = torch.empty((V, Dp), dtype=grad_dtype, device=dev)
     db = torch.empty((V,), dtype=torch.float32, device=dev)
     lib = _lib.load()

@@ -14,12 +14,14 @@ sm_100a kernels.
 
 from __future__ import annotations
 
+import ctypes
 from typing import Callable
 
 import torch
 import torch.distributed as dist
 
-from .head import sparton_backward, sparton_forward
+from . import _lib
+from .head import _stream_ptr, sparton_backward, sparton_forward
 
 
 def shard_range(V: int, world: int, rank: int) -> tuple[int, int, int]:
@@ -182,8 +184,74 @@ class FusedVocabGather:
         return self.Y, self.I
 
 
+class PeerDHReduce:
+    """The partial-dH sum of the sharded head in one kernel over NVLink peer
+    memory (``sparton_allreduce_peers``) instead of an NCCL
+    all-reduce.
+
+    Every rank owns a fp32 partial buffer ``part`` (the backward writes its
+    shard's dH contribution straight into it, ``out_dH``) and an output buffer
+    ``out`` in the gradient dtype, both addressable by every rank.  ``reduce``
+    runs barrier → kernel → barrier on the current stream: rank r sums its
+    slice of every rank's partial in rank order (deterministic, identical on
+    all ranks, the fp32 accumulation of the reference) and stores it — fp32,
+    or bf16 rounded once — into every rank's ``out``.  With ``multicast``
+    (NVLS) the sum is one ``multimem.ld_reduce`` per 16 bytes and the store
+    one ``multimem.st`` (``sparton_allreduce_multimem``).
+
+    ``PeerDHReduce.symmetric(shape, dtype, device, group)`` is the production
+    constructor (torch symmetric memory and its device barrier); the plain
+    constructor takes already-mapped peer addresses (rank order, own
+    included) and a barrier callable (the one-GPU test maps them by CUDA IPC)."""
+
+    def __init__(self, part: torch.Tensor, out: torch.Tensor, part_ptrs, out_ptrs, rank: int,
+                 barrier: Callable[[int], None], keepalive=(), multicast: tuple[int, int] | None = None):
+        if part.dtype != torch.float32 or out.shape != part.shape or out.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("part must be float32 and out float32/bfloat16 of the same shape")
+        if len(part_ptrs) != len(out_ptrs) or not 1 <= len(part_ptrs) <= 8 or not 0 <= rank < len(part_ptrs):
+            raise ValueError("one (part, out) address pair per rank, 1..8 ranks")
+        if part.numel() % 4:
+            raise ValueError("the reduced buffer must hold a multiple of 4 elements")
+        self.part, self.out, self.rank, self.barrier = part, out, rank, barrier
+        self.world = len(part_ptrs)
+        self._parts = (ctypes.c_void_p * self.world)(*[int(p) for p in part_ptrs])
+        self._outs = (ctypes.c_void_p * self.world)(*[int(p) for p in out_ptrs])
+        self.multicast = None if multicast is None else (int(multicast[0]), int(multicast[1]))
+        self._keepalive = keepalive
+
+    @classmethod
+    def symmetric(cls, shape, dtype, device, group=None, multicast: bool | None = False) -> "PeerDHReduce":
+        """``multicast`` as ``FusedVocabGather.symmetric``: False = P2P loads
+        and stores, True = require NVLS, None = NVLS when mapped."""
+        import torch.distributed._symmetric_memory as symm_mem
+        world, rank = _world(group)
+        grp = group if group is not None else dist.group.WORLD
+        part = symm_mem.empty(tuple(shape), dtype=torch.float32, device=device)
+        out = symm_mem.empty(tuple(shape), dtype=dtype, device=device)
+        hp = symm_mem.rendezvous(part, grp)
+        ho = symm_mem.rendezvous(out, grp)
+        return cls(part, out, [hp.buffer_ptrs[r] for r in range(world)], [ho.buffer_ptrs[r] for r in range(world)],
+                   rank, lambda ch: hp.barrier(channel=ch), keepalive=(hp, ho),
+                   multicast=FusedVocabGather.pick_multicast(hp, ho, multicast))
+
+    def reduce(self) -> torch.Tensor:
+        lib = _lib.load()
+        od = _lib.SPARTON_BF16 if self.out.dtype == torch.bfloat16 else _lib.SPARTON_F32
+        self.barrier(0)                       # every rank's partial is written
+        with torch.cuda.device(self.part.device):
+            if self.multicast is not None:
+                rc = lib.sparton_allreduce_multimem(self.multicast[0], self.multicast[1], self.world, self.rank, od,
+                                                    self.part.numel(), _stream_ptr())
+            else:
+                rc = lib.sparton_allreduce_peers(self._parts, self._outs, self.world, self.rank, od,
+                                                 self.part.numel(), _stream_ptr())
+        _lib.check(rc)
+        self.barrier(1)                       # every rank's slice has landed in our `out`
+        return self.out
+
+
 def local_backward(H, E_shard, Y_p, I_p, dY_p, *, grad_dtype=torch.float32, include_bias_grad=True,
-                   group=None, local_bwd: Callable | None = None):
+                   group=None, local_bwd: Callable | None = None, dh_reduce: PeerDHReduce | None = None):
     """Shard-local K2/K3, then the all-reduce of the partial dH (fp32).
 
     ``dY_p`` may be the column slice ``dY[:, v0:v1]`` of the replicated dY
@@ -194,6 +262,23 @@ def local_backward(H, E_shard, Y_p, I_p, dY_p, *, grad_dtype=torch.float32, incl
     in fp32 (the reference accumulates in fp32), then cast to ``grad_dtype``
     (``reduce_dh``: reduce-scatter, cast, all-gather for a bf16 result)."""
     world, _ = _world(group)
+    if dh_reduce is not None:
+        # Partial dH straight into the peer-addressable buffer; the reduction
+        # kernel runs on the communication stream once dH is final, beside dE.
+        main = torch.cuda.current_stream(H.device)
+        ready = torch.cuda.Event()
+        _, dE, db = sparton_backward(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
+                                     grad_dtype=torch.float32, dh_ready=ready, out_dH=dh_reduce.part)
+        if dh_reduce.out.dtype != grad_dtype:
+            raise ValueError(f"dh_reduce produces {dh_reduce.out.dtype}, asked for {grad_dtype}")
+        comm = _comm_stream(H.device)
+        comm.wait_event(ready)
+        with torch.cuda.stream(comm):
+            dH = dh_reduce.reduce()
+        main.wait_stream(comm)
+        if grad_dtype != torch.float32:
+            dE = dE.to(grad_dtype)
+        return dH, dE, db
     if local_bwd is not None or not H.is_cuda or world == 1:
         fn = local_bwd or sparton_backward
         dH, dE, db = fn(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,

@@ -26,7 +26,7 @@ def test_header_declares_entry_points():
                             "sparton_quantize_e4m3",
                             "sparton_bwd_workspace_bytes", "sparton_bwd", "sparton_bwd_ex",
                             "sparton_bwd_fp8", "sparton_mx_scales_bytes", "sparton_quantize_mx",
-                            "sparton_fwd_mx"])
+                            "sparton_fwd_mx", "sparton_allreduce_peers", "sparton_allreduce_multimem"])
 
 
 def test_library_exports_every_declared_symbol():
@@ -173,3 +173,26 @@ def test_staged_de_sequence_limit():
         extra = up(B * (V + V % 2) * 8) if staged else up(V * D * 4)
         assert lib.sparton_bwd_workspace_bytes(B, S, D, V, _lib.SPARTON_F32) == base + (
             extra if staged else 0) + 256, S
+
+
+def test_allreduce_entry_points_reject_bad_arguments_before_any_cuda_call():
+    """sparton_allreduce_peers / _multimem validate ranks, dtype, n and
+    pointers on the host (EINVAL) before touching the device."""
+    from paper_2603_25011_b200 import _lib
+    lib = _lib.load()
+    d = 0x1000
+    arr = (ctypes.c_void_p * 2)(d, d)
+    F32, BF16 = _lib.SPARTON_F32, _lib.SPARTON_BF16
+    assert lib.sparton_allreduce_peers(arr, arr, 0, 0, F32, 8, None) == _lib.SPARTON_EINVAL      # nranks
+    assert lib.sparton_allreduce_peers(arr, arr, 9, 0, F32, 8, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_allreduce_peers(arr, arr, 2, 2, F32, 8, None) == _lib.SPARTON_EINVAL      # rank
+    assert lib.sparton_allreduce_peers(arr, arr, 2, 0, 7, 8, None) == _lib.SPARTON_EINVAL        # dtype
+    assert lib.sparton_allreduce_peers(arr, arr, 2, 0, F32, 6, None) == _lib.SPARTON_EINVAL      # n % 4
+    assert lib.sparton_allreduce_peers(None, arr, 2, 0, F32, 8, None) == _lib.SPARTON_EINVAL
+    odd = (ctypes.c_void_p * 2)(d, d + 4)
+    assert lib.sparton_allreduce_peers(odd, arr, 2, 0, F32, 8, None) == _lib.SPARTON_EINVAL      # alignment
+    assert lib.sparton_allreduce_peers(arr, odd, 2, 0, BF16, 8, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_allreduce_multimem(d, d, 2, 0, F32, 6, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_allreduce_multimem(None, d, 2, 0, F32, 8, None) == _lib.SPARTON_EINVAL
+    assert lib.sparton_allreduce_multimem(d, d + 8, 2, 0, F32, 8, None) == _lib.SPARTON_EINVAL
+    assert "aligned" in lib.sparton_last_error().decode()

@@ -19,4 +19,6 @@ for tool in ${TOOLS:-memcheck racecheck synccheck}; do
   # gathered dE (S > 832) and packed short sequences
   run gathered $tool python tools/sanitize_case.py 3 1000 256 20000
   run packed $tool python tools/sanitize_case.py 16 48 128 5000 0 mx
+  # the peer-memory dH reduction kernel
+  run allreduce $tool python tools/sanitize_allreduce.py
 done
