@@ -101,12 +101,35 @@ def _precision() -> str:
     return PRECISION
 
 
+_STAGE_BYTES = 64 << 20
+
+
 def _upload(x: np.ndarray, dev, precision: str | None = None, dtype=np.float32) -> torch.Tensor:
-    """Host array -> device tensor through a pinned staging copy (torch's
-    caching host allocator): ~47 GB/s memcpy + ~56 GB/s DMA on the B200 box
-    vs ~11 GB/s for a pageable copy (tools/xfer_probe.py).  bf16 conversion
-    happens on the device."""
-    t = torch.from_numpy(np.ascontiguousarray(x, dtype=dtype)).pin_memory().to(dev, non_blocking=True)
+    """Host array -> device tensor through pinned staging (torch's caching
+    host allocator): ~47 GB/s memcpy + ~56 GB/s DMA on the B200 box vs
+    ~11 GB/s for a pageable copy (tools/xfer_probe.py).  Arrays above 64 MB
+    go in 64 MB chunks through two pinned buffers, so the host copy of chunk
+    k+1 overlaps the DMA of chunk k.  bf16 conversion happens on the device."""
+    src = torch.from_numpy(np.ascontiguousarray(x, dtype=dtype))
+    if src.numel() * src.element_size() <= _STAGE_BYTES:
+        t = src.pin_memory().to(dev, non_blocking=True)
+    else:
+        t = torch.empty(src.shape, dtype=src.dtype, device=dev)
+        flat, dst = src.reshape(-1), t.view(-1)
+        per = _STAGE_BYTES // src.element_size()
+        stage = [torch.empty(per, dtype=src.dtype, pin_memory=True) for _ in range(2)]
+        done = [None, None]
+        stream = torch.cuda.current_stream(dev)
+        for k, i0 in enumerate(range(0, flat.numel(), per)):
+            i1 = min(flat.numel(), i0 + per)
+            buf = stage[k % 2]
+            if done[k % 2] is not None:
+                done[k % 2].synchronize()            # the DMA that read this buffer has finished
+            buf[:i1 - i0].copy_(flat[i0:i1])         # host copy (torch's parallel memcpy)
+            dst[i0:i1].copy_(buf[:i1 - i0], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done[k % 2] = ev
     return t if precision in (None, "fp32") else t.to(torch.bfloat16)
 
 
@@ -153,6 +176,29 @@ def _device_oom(tracker, nbytes: int, exc: BaseException) -> AllocationCapExceed
     return err
 
 
+def _check_layout(inputs) -> None:
+    """The shape/dtype half of HeadInputs.validate (reference.py:30-41), with
+    its messages, in its order; the value half runs on the device
+    (``_check_values``) instead of four numpy passes over the host arrays."""
+    d = inputs.dims
+    for name, want, dt in (("H", (d.B, d.S, d.D), np.float32), ("E", (d.V, d.D), np.float32),
+                           ("b", (d.V,), np.float32), ("mask", (d.B, d.S), np.uint8)):
+        a = getattr(inputs, name)
+        if a.shape != want or a.dtype != dt:
+            raise ValueError(f"{name} must be {np.dtype(dt).name} {want}, got {a.dtype} {a.shape}")
+
+
+def _check_values(H: torch.Tensor, E: torch.Tensor, b: torch.Tensor, m: torch.Tensor) -> None:
+    """The value half of HeadInputs.validate (reference.py:42-46, tensor.py:118-120)
+    on the uploaded fp32 / uint8 tensors: same checks, same order, same
+    ValueError messages."""
+    for name, t in (("H", H), ("E", E), ("b", b)):
+        if not bool(torch.isfinite(t).all()):
+            raise ValueError(f"{name} contains NaN or Inf")
+    if not bool((m <= 1).all()):
+        raise ValueError("mask values must be exactly 0 or 1")
+
+
 def _run_forward(inputs, tracker) -> HeadOutput:
     dev = _device()
     d = inputs.dims
@@ -160,10 +206,13 @@ def _run_forward(inputs, tracker) -> HeadOutput:
     with _Charge(tracker, nbytes):
         try:
             prec = _precision()
-            H = _upload(inputs.H, dev, prec)
-            E = _upload(inputs.E, dev, prec)
+            Hf = _upload(inputs.H, dev)
+            Ef = _upload(inputs.E, dev)
             b = _upload(inputs.b, dev)
             m = _upload(inputs.mask, dev, dtype=np.uint8)
+            _check_values(Hf, Ef, b, m)
+            H, E = (Hf, Ef) if prec == "fp32" else (Hf.to(torch.bfloat16), Ef.to(torch.bfloat16))
+            del Hf, Ef
             Y, I = (sparton_forward_fp32 if prec == "fp32" else sparton_forward)(H, E, b, m)
             Yh, Ih = _download(Y, I)
             out = HeadOutput(Y=Yh, I=Ih)
@@ -175,8 +224,10 @@ def _run_forward(inputs, tracker) -> HeadOutput:
 
 
 def forward_hybrid(inputs, cfg=None, tracker=None) -> HeadOutput:
-    """Drop-in for fused.forward_hybrid (fused.py:115-157) on the B200 kernel."""
-    inputs.validate()
+    """Drop-in for fused.forward_hybrid (fused.py:115-157) on the B200 kernel.
+    ``inputs`` are validated as HeadInputs.validate does — layout on the host,
+    finiteness and mask values on the device after the upload."""
+    _check_layout(inputs)
     (cfg or TileConfig.default_for(inputs.dims)).validate_for(inputs.dims)
     return _run_forward(inputs, tracker)
 
@@ -184,7 +235,7 @@ def forward_hybrid(inputs, cfg=None, tracker=None) -> HeadOutput:
 def forward_fully_fused(inputs, cfg=None, tracker=None) -> HeadOutput:
     """Drop-in for fused.forward_fully_fused (fused.py:160-212): on B200 the
     streaming reduction and the hybrid are the same single fused kernel."""
-    inputs.validate()
+    _check_layout(inputs)
     (cfg or TileConfig.default_for(inputs.dims)).validate_for(inputs.dims)
     return _run_forward(inputs, tracker)
 

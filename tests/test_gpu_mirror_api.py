@@ -95,6 +95,41 @@ def test_mirror_reference_errors(cuda_device):
         fh.backward_fused(x, fh.SavedSparseState.from_output(out), np.zeros((2, 4), np.float32))
 
 
+def test_mirror_validation_messages_match_reference_validate(cuda_device):
+    """The drop-in checks layout on the host and values on the device, with
+    the exact ValueError of the reference's HeadInputs.validate
+    (reference.py:30-46) for every failure, in the same precedence."""
+    from paper_2603_25011_b200 import fusedhead as fh
+    x = _inputs(2, 3, 8, 5, seed=2)
+
+    def variant(**kw):
+        f = {"H": x.H.copy(), "E": x.E.copy(), "b": x.b.copy(), "mask": x.mask.copy()}
+        f.update(kw)
+        return fh.HeadInputs(x.dims, f["H"], f["E"], f["b"], f["mask"])
+
+    def poke(a, idx, val):
+        a = a.copy()
+        a[idx] = val
+        return a
+
+    cases = [
+        variant(H=x.H[:, :2]), variant(H=x.H.astype(np.float64)), variant(E=x.E.T.copy()),
+        variant(b=x.b[:4]), variant(mask=x.mask.astype(np.int32)),
+        variant(H=poke(x.H, (1, 2, 3), np.nan)), variant(E=poke(x.E, (4, 0), np.inf)),
+        variant(b=poke(x.b, 2, -np.inf)), variant(mask=poke(x.mask, (0, 1), 3)),
+        # several faults at once: the first in the reference's order wins
+        variant(H=poke(x.H, (0, 0, 0), np.nan), E=poke(x.E, (0, 0), np.nan), mask=poke(x.mask, (0, 0), 2)),
+        variant(b=poke(x.b, 0, np.nan), mask=poke(x.mask, (0, 0), 2)),
+    ]
+    for bad in cases:
+        with pytest.raises(ValueError) as ref:
+            bad.validate()
+        for entry in (fh.forward_fully_fused, fh.forward_hybrid):
+            with pytest.raises(ValueError) as got:
+                entry(bad)
+            assert str(got.value) == str(ref.value)
+
+
 def test_mirror_zero_inputs_and_all_masked(cuda_device):
     # test_reference.py:33-39 (zeros -> Y = 0, I = 0) and :72-79 (all-masked row).
     from paper_2603_25011_b200 import fusedhead as fh
