@@ -4,7 +4,7 @@ set -e
 cd /root/repo
 name=$1; shift
 mkdir -p build/ab/obj_$name
-for s in sparton_abi sparton_fwd sparton_bwd; do
+for s in $(cd paper_2603_25011_b200/csrc && ls *.cu | sed "s/\.cu$//"); do
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr $@ -I include -c paper_2603_25011_b200/csrc/$s.cu -o build/ab/obj_$name/$s.o &
 done
 wait
