@@ -12,9 +12,10 @@ sys.path.insert(0, ".")
 from paper_2603_25011_b200.splade import EncoderConfig, SpladeTrainer, step_flops_head, synthetic_batch  # noqa: E402
 
 SQ, SD = int(sys.argv[1]) if len(sys.argv) > 1 else 64, int(sys.argv[2]) if len(sys.argv) > 2 else 256
-cfg = EncoderConfig()
+VOCAB = int(sys.argv[3]) if len(sys.argv) > 3 else 30522      # 250002: the XLM-R vocabulary (paper's 26x-batch case)
+cfg = EncoderConfig(vocab=VOCAB)
 for head in ("sparton", "naive"):
-    B = 64
+    B = 8 if VOCAB > 100000 else 64
     while B <= 8192:
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats()
@@ -32,12 +33,12 @@ for head in ("sparton", "naive"):
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / n
-            print(json.dumps({"head": head, "B": B, "Sq": SQ, "Sd": SD, "ms_per_step": ms,
+            print(json.dumps({"head": head, "V": VOCAB, "B": B, "Sq": SQ, "Sd": SD, "ms_per_step": ms,
                               "pairs_per_s": B / ms * 1e3, "peak_hbm_gb": torch.cuda.max_memory_allocated() / 1e9,
                               "head_tflops_alg": step_flops_head(B, SQ, SD, cfg) / ms / 1e9,
                               "loss": float(loss)}), flush=True)
         except torch.OutOfMemoryError:
-            print(json.dumps({"head": head, "B": B, "Sq": SQ, "Sd": SD, "result": "OOM"}), flush=True)
+            print(json.dumps({"head": head, "V": VOCAB, "B": B, "Sq": SQ, "Sd": SD, "result": "OOM"}), flush=True)
             break
         finally:
             tr = batch = None
