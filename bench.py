@@ -614,6 +614,27 @@ def gpu_cfg1(dev, steps, warmup):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
         rec[name] = {"ms_per_step": ms, "value": (ff + fb) / (ms * 1e-3) / 1e12}
+    # The bf16 step captured once in a CUDA graph and replayed: at this size the
+    # step is launch-bound, and graph replay removes the per-launch host work.
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        runs["bf16"]()
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        runs["bf16"]()
+    for _ in range(max(3, warmup)):
+        graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    rec["bf16_cuda_graph"] = {"ms_per_step": ms, "value": (ff + fb) / (ms * 1e-3) / 1e12}
     return rec
 
 
