@@ -265,12 +265,12 @@ def local_backward(H, E_shard, Y_p, I_p, dY_p, *, grad_dtype=torch.float32, incl
     if dh_reduce is not None:
         # Partial dH straight into the peer-addressable buffer; the reduction
         # kernel runs on the communication stream once dH is final, beside dE.
+        if dh_reduce.out.dtype != grad_dtype:
+            raise ValueError(f"dh_reduce produces {dh_reduce.out.dtype}, asked for {grad_dtype}")
         main = torch.cuda.current_stream(H.device)
         ready = torch.cuda.Event()
         _, dE, db = sparton_backward(H, E_shard, Y_p, I_p, dY_p, include_bias_grad=include_bias_grad,
                                      grad_dtype=torch.float32, dh_ready=ready, out_dH=dh_reduce.part)
-        if dh_reduce.out.dtype != grad_dtype:
-            raise ValueError(f"dh_reduce produces {dh_reduce.out.dtype}, asked for {grad_dtype}")
         comm = _comm_stream(H.device)
         comm.wait_event(ready)
         with torch.cuda.stream(comm):
