@@ -116,6 +116,12 @@ def _close(a, b, rtol, atol):
     # active, so the backward takes its sparse-regime kernels (per-pair dE
     # gathers, single-pass dH).
     ("cfg3_sparse", (512, 512, 768, 250002), 0.0, 1.0, -2.0),
+    # SPLADE query-length batches: packed short sequences (4 batch rows per
+    # 256-position chunk; S = 48 groups straddle batch rows) and a narrow
+    # last chunk (S = 300 = 256 + 44), all at the XLM-R vocabulary.
+    ("queries_S64_packed", (2048, 64, 768, 250002), 0.1, 0.9, 0.0),
+    ("queries_S48_straddling", (1024, 48, 768, 250002), 0.1, 0.9, 0.0),
+    ("docs_S300_narrow_chunk", (512, 300, 768, 250002), 0.1, 0.9, 0.0),
 ])
 def test_fullsize_forward_backward_vs_torch_fp32(cuda_device, name, dims, bias_std, keep, bias_mean):
     from paper_2603_25011_b200 import sparton_backward, sparton_forward
