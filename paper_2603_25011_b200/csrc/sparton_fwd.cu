@@ -607,7 +607,7 @@ sparton_fwd_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constan
 
 template <int CG, int NP, int OP>
 int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const CUtensorMap& tmSFA,
-                    const CUtensorMap& tmSFB, const FwdParams& prm, int num_sms, cudaStream_t stream) {
+                    const CUtensorMap& tmSFB, FwdParams prm, int num_sms, cudaStream_t stream) {
   using C = FwdCfg<CG, NP, OP>;
   constexpr int CL = CG * NP;   // cluster size
   auto kern = sparton_fwd_kernel<CG, NP, OP>;
@@ -650,6 +650,27 @@ int launch_fwd_impl(const CUtensorMap& tmE, const CUtensorMap& tmH, const CUtens
   if (want < grid / CL) grid = (int)want * CL;
   if (grid < CL) grid = CL;
   cfg.gridDim = dim3(grid, 1, 1);
+  {
+    // E group = one vocab tile per resident cluster: the round-robin over
+    // (group, b, tile) then hands cluster c tile c of every batch row, so a
+    // wave of units covers exactly one batch row (its H[b] read by every
+    // cluster at once) and each cluster keeps its E tile for the whole group.
+    // Measured against the former fixed 48 MB groups (128 tiles at D = 768):
+    // -2.5 ms per cfg3 step (paired in-step A/B on two boxes, the forward's
+    // lower energy buys clock) and less DRAM traffic
+    // (profiles/r02_fwd_experiments.txt).  Capped at 48 MB of E for wide D;
+    // a vocabulary whose whole E fits under the cap stays one group (H then
+    // streams once: V = 30522 measured 0.9 % faster that way).
+    const long long tile_bytes = (long long)C::TILE_V * prm.D * C::EB;
+    const long long cap = 48ll << 20;
+    int gv = grid / CL;
+    if ((long long)prm.num_vt * tile_bytes <= cap) gv = prm.num_vt;
+    if ((long long)gv * tile_bytes > cap) gv = (int)(cap / (tile_bytes > 0 ? tile_bytes : 1));
+    if (const char* ev = dev_env("SPARTON_FWD_GROUP_KB")) gv = (int)((atoll(ev) << 10) / (tile_bytes > 0 ? tile_bytes : 1));
+    if (gv < 1) gv = 1;
+    if (gv > prm.num_vt) gv = prm.num_vt;
+    prm.group_vt = gv;
+  }
   e = cudaLaunchKernelEx(&cfg, kern, tmE, tmH, tmSFA, tmSFB, prm);
   if (e != cudaSuccess) return set_cuda_error("launch sparton_fwd_kernel", e);
   return SPARTON_OK;
@@ -685,15 +706,10 @@ int launch_fwd(const CUtensorMap& tmE, const CUtensorMap& tmH, const CUtensorMap
   if (prm.num_units >= (1ll << 31) - 4096)
     return set_error(SPARTON_EINVAL, "B * ceil(V / vocab_tile) exceeds the forward scheduler's 31-bit unit index");
   const int nclusters = max(1, num_sms / cluster_ctas);
-  // E group of ~48 MB stays L2-resident while H streams (see UnitIter);
-  // 48 MB measured lower DRAM traffic than 4-32 MB (profiles/r01_fwd_l2_policy.txt).
-  const long long tile_bytes = (long long)tile_v * prm.D * (prm.fp8 ? 1 : 2);
-  long long group_bytes = 48ll << 20;
-  if (const char* ev = dev_env("SPARTON_FWD_GROUP_KB")) group_bytes = atoll(ev) << 10;
-  int gv = (int)(group_bytes / (tile_bytes > 0 ? tile_bytes : 1));
-  if (gv < 1) gv = 1;
-  if (gv > prm.num_vt) gv = prm.num_vt;
-  prm.group_vt = gv;
+  // E group (vocab tiles walked for every batch row before the next group,
+  // see UnitIter): set per launch in launch_fwd_impl, once the number of
+  // resident clusters is known.
+  prm.group_vt = 0;
   // Epilogue experiment switch (1-3: max-only variants with WRONG I, 4: the
   // per-element strict '>' scan) — honoured only in a SPARTON_DEV=1 process.
   prm.epi_mode = 0;

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("libs", nargs="+")
 ap.add_argument("--rounds", type=int, default=4)
 ap.add_argument("--steps", type=int, default=10)
+ap.add_argument("--shape", default="512,512,768,250002", help="B,S,D,V")
 args = ap.parse_args()
 names = args.libs
 libs = [ctypes.CDLL(p) for p in names]
@@ -28,7 +29,7 @@ for lib in libs:
     lib.sparton_bwd_workspace_bytes.restype = ctypes.c_size_t
     lib.sparton_bwd.argtypes = [vp] * 8 + [i64] * 6 + [ci, ci, vp, ctypes.c_size_t, vp]
 
-B, S, D, V = 512, 512, 768, 250002
+B, S, D, V = (int(x) for x in args.shape.split(","))
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(0)
 H = torch.randn((B, S, D), generator=g, device=dev).to(torch.bfloat16)
